@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the PlenOctree render hot path (BASELINE.json metric: 800x800 FPS and
+Mrays/s, SH-3 512^3 PlenOctree, 1/2/4/8 B200, % of HBM peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one 800x800 frame of config c1 (depth-9 sparse octree, SH-3, fp32 payload,
+gamma = 0.01) through po_render, inputs resident in HBM.  Views walk the c1 orbit
+(az = 37 + 1.8 i deg) so consecutive steps render different frames, and L2 is flushed
+(a 256 MiB write) before every timed step; each step is timed with CUDA events on the
+launching stream and only the render is inside the events.  For N > 1 (torchrun) every
+rank renders its own views (weak scaling, tree replicated, no collective in the timed
+region) and the time is the max over ranks.
+
+`--impl reference` times the CPU oracle (oracle/, double precision, OpenMP) on a bounded
+sample of the same workload on this host's cores: the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W = H = 800
+GAMMA = 0.01
+METRIC = "800x800 FPS, SH-3 512^3 PlenOctree (c1)"
+UNIT = "frames/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _ncu_traffic():
+    """dram bytes per k_render launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_render_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        return float(s["dram_bytes_per_launch"]), s.get("source", path)
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        import statistics
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _workload_desc(tree_gen):
+    return {"workload": "c1: NeRF-synthetic-shaped SDF object, depth-9 sparse octree (512^3), "
+                        f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp32 payload, 800x800, gamma 0.01",
+            "views": "c1 orbit, az = 37 + 1.8*i deg, el 30 deg, r 3.4, f 1111.1 px; rank r renders views r, r+N, ...",
+            "l2": "flushed (256 MiB write) before every timed step; only the render is inside the CUDA events",
+            "global_batch": "1 frame per rank per step"}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import gen
+    import paper_2103_14024_b200 as po
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    po.lib()
+    t_gen = gen.scene_c1()
+    tree = po.tree_from_gen(t_gen, device=local)
+    n_views = max(args.steps + args.warmup, 1) * ws
+    cam_recs = np.concatenate([gen.config_camera("c1", v)[0] for v in range(n_views)])
+    cams = po.cams_tensor(cam_recs, dev)
+    out = torch.empty((1, H, W, 3), dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def view_of(step):
+        return (step * ws + rank) % n_views
+
+    # algorithmic bytes per launch: counters of the same traversal
+    B = t_gen.basis_dim
+    row_bytes = 3 * B * 4
+    stats = {"leaf_visits": 0, "sh_rows": 0, "nodes": 0, "hit_rays": 0}
+    for s in range(args.warmup, args.warmup + args.steps):
+        v = view_of(s)
+        st = po.po_render_stats(tree, cams[v:v + 1], W, H, gamma=GAMMA)
+        for k in stats:
+            stats[k] += st[k]
+    K = max(args.steps, 1)
+    alg_bytes = (stats["leaf_visits"] * 4 + stats["sh_rows"] * row_bytes + stats["nodes"] * 32) / K + W * H * 12 + 64
+
+    for s in range(args.warmup):
+        flush.zero_()
+        po.po_render(tree, cams[view_of(s):view_of(s) + 1], W, H, out=out, gamma=GAMMA)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = po.launch_count()
+    evs = []
+    for s in range(args.warmup, args.warmup + args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        v = view_of(s)
+        e0.record(stream)
+        po.po_render(tree, cams[v:v + 1], W, H, out=out, gamma=GAMMA)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    launches = po.launch_count() - l0
+    clk = clocks.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t_max = t_ms
+    if ws > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ms_per_step = t_max / K
+    fps = ws * K / (t_max / 1e3)
+    kernel_ms = t_ms / K   # one kernel launch per step
+
+    # e2e: the same frames through the host-buffer C-ABI entry point (H2D cameras, D2H image)
+    pinned = torch.empty((1, H, W, 3), dtype=torch.float32, pin_memory=True).numpy()
+    e2e_ms = 0.0
+    e2e_steps = min(K, 50)
+    for s in range(2):
+        po.po_render_host(tree, cam_recs[view_of(s):view_of(s) + 1], W, H, out_host=pinned, gamma=GAMMA)
+    if ws > 1:
+        torch.distributed.barrier()
+    for s in range(args.warmup, args.warmup + e2e_steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        v = view_of(s)
+        e0.record(stream)
+        po.po_render_host(tree, cam_recs[v:v + 1], W, H, out_host=pinned, gamma=GAMMA)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    if ws > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_fps = ws * e2e_steps / (e2e_ms / 1e3)
+
+    if rank == 0:
+        peak, peak_src = _peaks()
+        achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+        traffic, tsrc = _ncu_traffic()
+        line = {
+            "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural SDF scene, seeded)",
+            "config": _workload_desc(t_gen) | {"parallelism": f"view-sharded x{ws}, tree replicated"},
+            "mrays_per_s": round(fps * W * H / 1e6, 1),
+            "leaf_visits_per_frame": stats["leaf_visits"] / K,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "po::k_render<3,false>", "peak_source": peak_src,
+                         "alg_bytes_per_launch": round(alg_bytes),
+                         "alg_bytes_def": "leaf visits*4 B sigma + SH rows*192 B + internal nodes met*32 B + 12 B/pixel out",
+                         "traffic_source": tsrc},
+            "e2e": {"value": round(e2e_fps, 2), "unit": UNIT, "h2d_bytes_per_step": 64,
+                    "d2h_bytes_per_step": W * H * 12, "entry": "po_render_host (host cameras -> host image)"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline and ws == 1:
+            line["cpu_baseline"] = cpu_baseline(t_gen, seconds=args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(t_gen, seconds: float = 15.0, max_frames: int = 200):
+    """The oracle as it stands, on this host's cores, on whole c1 frames (bounded by ~seconds)."""
+    import numpy as np
+    import gen
+    import oracle
+    oracle.build()
+    ot = oracle.OracleTree(t_gen)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    frames = 0
+    while frames < max_frames and (time.perf_counter() - t0) < seconds:
+        cam, _, _ = gen.config_camera("c1", frames)
+        rays = oracle.camera_rays(cam, W, H)
+        oracle.render(ot, rays, gamma=GAMMA, nthreads=cores)
+        frames += 1
+    dt = time.perf_counter() - t0
+    return {"value": round(frames / dt, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{frames} full c1 frames (views 0..{frames - 1}), ray generation + render, double precision, "
+                      f"OpenMP {cores} threads, {dt:.1f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import gen
+    t_gen = gen.scene_c1()
+    # each step = a bounded sample of one c1 frame: every 4th pixel row (rows j = s mod 4),
+    # 160,000 rays, ~0.1-0.3 s of CPU work; value is scaled to whole frames per second
+    import oracle
+    oracle.build()
+    ot = oracle.OracleTree(t_gen)
+    cores = os.cpu_count() or 1
+    frac = 0.25
+
+    def step(s):
+        cam, _, _ = gen.config_camera("c1", s)
+        rays = oracle.camera_rays(cam, W, H).reshape(H, W, 6)[s % 4::4].reshape(-1, 6)
+        oracle.render(ot, rays, gamma=GAMMA, nthreads=cores)
+
+    for s in range(args.warmup):
+        step(s)
+    t0 = time.perf_counter()
+    for s in range(args.warmup, args.warmup + args.steps):
+        step(s)
+    dt = time.perf_counter() - t0
+    v = frac * args.steps / dt
+    sample = (f"{args.steps} steps x 1/4 of a c1 frame (every 4th row, 160k rays incl. ray generation), "
+              f"double precision, OpenMP {cores} threads, {dt:.1f} s")
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (procedural SDF scene, seeded)", "config": _workload_desc(t_gen),
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/* =====================================================================================
+ *  libplenoct -- C ABI of the B200 PlenOctree rendering hot path (forward + analytic
+ *  backward).  PAPER.md = arXiv 2103.14024 source, cited as P:<line>; SURVEY.md §8(b)
+ *  lists these entry points.  Readings of the paper (Q1..Q32) are in DESIGN.md.
+ *
+ *  Conventions shared by every call
+ *  - Status codes, never exceptions.  On a non-OK status po_last_error() returns a
+ *    thread-local message naming the failing argument / index.
+ *  - "device" pointers are CUDA device pointers on the tree's device; "host" pointers
+ *    are ordinary (pageable or pinned) host memory.  The library never keeps a pointer
+ *    it was given after the call returns (device calls: after the stream work is done).
+ *  - po_stream is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *    render / backward / update calls are asynchronous on that stream; the caller
+ *    orders them (e.g. po_tree_sgd_step after every render that reads the tree).
+ *  - CUDA launch and asynchronous errors map to PO_ERR_CUDA (a sticky error from an
+ *    earlier kernel is reported by the next call that checks).
+ *  - There is NO CPU fallback: every compute call runs CUDA kernels for sm_100a.
+ * ===================================================================================== */
+#ifndef PLENOCT_H_
+#define PLENOCT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PO_OK = 0,
+    PO_ERR_INVALID_ARG = 1,   /* bad size, NULL where required, non-orthonormal camera, ... */
+    PO_ERR_INVALID_TREE = 2,  /* malformed child table, NaN/Inf payload, leaf deeper than D  */
+    PO_ERR_OOM = 3,           /* cudaMalloc failed                                           */
+    PO_ERR_CUDA = 4,          /* any other CUDA runtime error                                */
+    PO_ERR_UNSUPPORTED = 5    /* sh_degree > 3, unknown payload, op not defined for payload  */
+} po_status;
+
+enum { PO_F32 = 0, PO_F16 = 1 };          /* leaf SH payload precision (sigma~ is always f32, reading Q20) */
+enum { PO_SH_CS = 0, PO_SH_NO_CS = 1 };   /* real-SH sign convention (reading Q16; default CS)          */
+
+typedef void* po_stream;                  /* cudaStream_t */
+typedef struct po_tree po_tree;           /* opaque; owns the device copy of the tree */
+
+/* Tree geometry and payload format ("stores density and SH coefficients at each
+ * leaf"; cube bbox, reading Q4).  Leaf grid = 2^max_depth cells per axis. */
+typedef struct {
+    float bbox_min[3];
+    float bbox_edge;      /* > 0, world units                                  */
+    int32_t max_depth;    /* D, 1..15                                          */
+    int32_t sh_degree;    /* l_max, 0..3 ; B = (l_max+1)^2 coefficients/channel */
+    int32_t payload;      /* PO_F32 | PO_F16                                   */
+    int32_t sh_sign;      /* PO_SH_CS | PO_SH_NO_CS                            */
+    int32_t device;       /* CUDA ordinal the tree lives on                    */
+} po_tree_desc;
+
+/* Pinhole camera (reading Q5): c2w = camera-to-world 3x4 (OpenGL axes: x right, y up,
+ * -z forward; the 3x3 block must be orthonormal within 1e-4), focal lengths and principal
+ * point in pixels.  Pixel (i, j), row 0 at the top, shoots through its centre:
+ * d_cam = ((i+0.5-cx)/fx, -(j+0.5-cy)/fy, -1), d = normalize(R d_cam), o = c2w[:,3]. */
+typedef struct {
+    float c2w[3][4];
+    float fx, fy, cx, cy;
+} po_camera;
+
+/* gamma: early-stop threshold on transmittance, P:435-437 (0 disables; default 0.01).
+ * background: c_N, the background light intensity of App. B.3 P:855-868 (default white). */
+typedef struct {
+    float gamma;
+    float background[3];
+} po_render_opts;
+
+const char* po_last_error(void);
+const char* po_version(void);
+
+/* ---- a0: tree upload ---------------------------------------------------------------
+ * child  host uint32[n_nodes][8]: entry = tag<<30 | index, tag 0 empty, 1 internal node,
+ *        2 leaf (reading Q1); octant = 4*bx + 2*by + bz (reading Q2); node 0 is the root.
+ * sigma  host float[n_leaves]: sigma~ (pre-ReLU density per world unit).
+ * sh     host float[n_leaves][B][3]: k_l^m per RGB channel, (l,m) lexicographic with
+ *        m = -l..l, basis-major / channel-minor (reading Q17).  Converted to
+ *        fp16 (round to nearest even) when desc->payload == PO_F16.
+ * Validates: every index in range and referenced at most once, every node reachable,
+ * leaves no deeper than D, finite payload (else PO_ERR_INVALID_TREE).  Synchronous.
+ * The caller keeps ownership of the host arrays; *out owns device memory until
+ * po_tree_destroy. */
+po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_t n_nodes, const float* sigma,
+                         const float* sh, int64_t n_leaves, po_tree** out);
+po_status po_tree_destroy(po_tree* tree);
+/* sh_row_bytes: padded device row of one leaf's SH payload (16-byte multiple). */
+po_status po_tree_info(const po_tree* tree, int64_t* n_nodes, int64_t* n_leaves, int32_t* sh_row_bytes);
+/* Copy the current leaf values back (host float sigma[n_leaves], sh[n_leaves][B][3]; either may
+ * be NULL).  Synchronous (device-wide sync of the tree's device). */
+po_status po_tree_read_leaves(const po_tree* tree, float* sigma, float* sh);
+
+/* ---- a1..a6: forward render (Eq. 1-2, Eq. 5) ----------
+ * cams     device po_camera[n_cams]
+ * out_rgb  device float[n_cams][H][W][3], fp32 linear RGB (reading Q30)
+ * For each pixel: ray generation, bbox clip (t_near = max(0, entry)), ordered octree
+ * descent over positive-length leaf segments, sigma = max(sigma~,0), alpha =
+ * 1-exp(-sigma delta), c = sigmoid(sum k Y(d)), C += T alpha c, stop once T < gamma
+ * (after compositing that segment, reading Q11), then C += T c_N. */
+po_status po_render(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                    const po_render_opts* opts, float* out_rgb, po_stream stream);
+
+/* Same as po_render with HOST cameras and a HOST output image: copies the cameras in,
+ * renders, copies the image out and synchronises the stream (end-to-end entry point). */
+po_status po_render_host(const po_tree* tree, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
+                         const po_render_opts* opts, float* out_rgb_host, po_stream stream);
+
+/* Forward render of explicit rays.
+ * rays     device float[n][6] = (origin xyz, direction xyz); the direction is normalised
+ *          by the library (zero direction => that ray returns the background).
+ * out_rgb  device float[n][3]
+ * aux      device double[n][4] or NULL: (C_r, C_g, C_b, T_final) accumulated in double;
+ *          po_render_backward uses it to skip its own first pass. */
+po_status po_render_rays(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
+                         float* out_rgb, double* aux, po_stream stream);
+
+/* ---- a7/a8: analytic backward (App. B.3: P:886-892 colour, P:938-947 density,
+ * P:949-957 two passes, P:959-963 ReLU) -----------------------------------------------
+ * dL_dC       device float[n][3], the loss gradient per ray (e.g. 2(C^ - C) for Eq. 3).
+ * aux         device double[n][4] from po_render_rays with the same tree/rays/opts, or NULL
+ *             (then the kernel runs its own first pass to get the total sum_k c_k w_k).
+ * grad_sigma  device float[n_leaves]      d L / d sigma~   (ACCUMULATED: +=)
+ * grad_sh     device float[n_leaves][B][3] d L / d k         (ACCUMULATED: +=)
+ * The caller zeroes the gradients; cross-ray summation order is nondeterministic.
+ * opts->gamma applies exactly as in the forward (gamma = 0 is the paper-literal optimiser,
+ * reading Q12). */
+po_status po_render_backward(const po_tree* tree, const float* rays, int64_t n, const float* dL_dC,
+                             const double* aux, const po_render_opts* opts, float* grad_sigma, float* grad_sh,
+                             po_stream stream);
+
+/* Eq. (3) helper: dL_dC[i] = 2 (pred[i] - target[i]) over n*3 floats; if loss != NULL,
+ * *loss (device double) = sum (pred - target)^2 (overwritten). */
+po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, float* dL_dC, double* loss,
+                          int32_t device, po_stream stream);
+
+/* a9 update: plain SGD on an fp32 tree, in place:
+ * sigma~ -= lr * grad_sigma, k -= lr * grad_sh.  PO_ERR_UNSUPPORTED for fp16 payloads. */
+po_status po_tree_sgd_step(po_tree* tree, const float* grad_sigma, const float* grad_sh, float lr,
+                           po_stream stream);
+
+/* ---- parity / measurement helpers ----------------------------------------------------
+ * po_trace: the visited-leaf sequence of each ray up to termination (same traversal as
+ * po_render_rays).  leaf_ids device int32[n][max_leaves] (first max_leaves, -1 padded;
+ * may be NULL when max_leaves == 0), counts device int32[n] (leaves composited, sigma~<=0
+ * leaves included, reading Q10), node_counts device int32[n] or NULL (internal nodes,
+ * root included, whose box the processed interval meets). */
+po_status po_trace(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
+                   int32_t max_leaves, int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, po_stream stream);
+
+/* po_render_stats: counters of the po_render traversal over n_cams views, ADDED to
+ * device uint64 counters[4] = {leaf visits, leaf visits with sigma~ > 0 (SH row read),
+ * internal nodes met (root included), rays that hit the bbox}. */
+po_status po_render_stats(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                          const po_render_opts* opts, unsigned long long* counters, po_stream stream);
+
+/* Number of kernel launches the library has issued since load (bench accounting). */
+int64_t po_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLENOCT_H_ */

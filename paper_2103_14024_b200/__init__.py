@@ -1,0 +1,294 @@
+"""B200-native PlenOctree rendering hot path (arXiv 2103.14024): thin Python binding.
+
+Every call marshals arguments to the C ABI of ``libplenoct.so`` (``include/plenoct.h``)
+and nothing else: all compute runs in the library's sm_100a CUDA kernels.  PyTorch is
+used only for device memory and streams.  If the shared library is missing the import
+fails loudly -- there is no CPU fallback.
+
+Names follow the C ABI: ``po_tree_create``, ``po_render``, ``po_render_host``,
+``po_render_rays``, ``po_render_backward``, ``po_l2_loss_grad``, ``po_tree_sgd_step``,
+``po_trace``, ``po_render_stats``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._build import LIB as _LIB_PATH
+
+PO_F32, PO_F16 = 0, 1
+PO_SH_CS, PO_SH_NO_CS = 0, 1
+STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_ERR_OOM", 4: "PO_ERR_CUDA",
+          5: "PO_ERR_UNSUPPORTED"}
+
+EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_destroy", "po_tree_info",
+           "po_tree_read_leaves", "po_render", "po_render_host", "po_render_rays", "po_render_backward",
+           "po_l2_loss_grad", "po_tree_sgd_step", "po_trace", "po_render_stats"]
+
+
+class PoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class TreeDesc(ctypes.Structure):
+    _fields_ = [("bbox_min", ctypes.c_float * 3), ("bbox_edge", ctypes.c_float), ("max_depth", ctypes.c_int32),
+                ("sh_degree", ctypes.c_int32), ("payload", ctypes.c_int32), ("sh_sign", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+class RenderOpts(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_float), ("background", ctypes.c_float * 3)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libplenoct.so (raises if it has not been built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(_LIB_PATH)
+        P, I32, I64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+        L.po_last_error.restype = ctypes.c_char_p
+        L.po_version.restype = ctypes.c_char_p
+        L.po_launch_count.restype = I64
+        L.po_tree_create.argtypes = [P, P, I64, P, P, I64, ctypes.POINTER(P)]
+        L.po_tree_destroy.argtypes = [P]
+        L.po_tree_info.argtypes = [P, P, P, P]
+        L.po_tree_read_leaves.argtypes = [P, P, P]
+        L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
+        L.po_render_host.argtypes = [P, P, I32, I32, I32, P, P, P]
+        L.po_render_rays.argtypes = [P, P, I64, P, P, P, P]
+        L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P]
+        L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
+        L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
+        L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, P]
+        L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
+        for name in EXPORTS:
+            if name not in ("po_last_error", "po_version", "po_launch_count"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise PoError(status, lib().po_last_error().decode())
+
+
+def _ptr(x):
+    """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _opts(gamma: float, background) -> RenderOpts:
+    bg = (ctypes.c_float * 3)(*[float(v) for v in background])
+    return RenderOpts(float(gamma), bg)
+
+
+def _need(t, dtype, shape_tail=None, cuda=True):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch tensor")
+    if cuda and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    if shape_tail is not None and tuple(t.shape[-len(shape_tail):]) != tuple(shape_tail):
+        raise ValueError(f"expected trailing shape {shape_tail}, got {tuple(t.shape)}")
+    return t
+
+
+class PlenOctree:
+    """Owner of a ``po_tree*`` (device copy of the tree)."""
+
+    def __init__(self, handle, desc: TreeDesc, n_nodes: int, n_leaves: int):
+        self._h = handle
+        self.desc = desc
+        self.n_nodes = n_nodes
+        self.n_leaves = n_leaves
+        self.sh_degree = desc.sh_degree
+        self.B = (desc.sh_degree + 1) ** 2
+        self.device = desc.device
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("tree destroyed")
+        return self._h
+
+    def info(self):
+        nn, nl, rb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        _check(lib().po_tree_info(self.handle, ctypes.byref(nn), ctypes.byref(nl), ctypes.byref(rb)))
+        return nn.value, nl.value, rb.value
+
+    def read_leaves(self):
+        sig = np.zeros(self.n_leaves, np.float32)
+        sh = np.zeros((self.n_leaves, self.B, 3), np.float32)
+        _check(lib().po_tree_read_leaves(self.handle, _ptr(sig), _ptr(sh)))
+        return sig, sh
+
+    def destroy(self):
+        if self._h is not None:
+            lib().po_tree_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def po_tree_create(child, sigma, sh, depth: int, sh_degree: int, bbox_min=(-1.0, -1.0, -1.0), edge: float = 2.0,
+                   payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0) -> PlenOctree:
+    """Upload a tree from host arrays (child uint32[n_nodes][8], sigma f32[n_leaves], sh f32[n_leaves][B][3])."""
+    child = np.ascontiguousarray(child, dtype=np.uint32).reshape(-1, 8)
+    sigma = np.ascontiguousarray(sigma, dtype=np.float32).reshape(-1)
+    B = (sh_degree + 1) ** 2
+    sh = np.ascontiguousarray(sh, dtype=np.float32).reshape(sigma.shape[0], B, 3)
+    desc = TreeDesc((ctypes.c_float * 3)(*[float(v) for v in bbox_min]), float(edge), int(depth), int(sh_degree),
+                    int(payload), int(sh_sign), int(device))
+    h = ctypes.c_void_p()
+    _check(lib().po_tree_create(ctypes.byref(desc), _ptr(child), child.shape[0], _ptr(sigma), _ptr(sh),
+                                sigma.shape[0], ctypes.byref(h)))
+    return PlenOctree(h, desc, child.shape[0], sigma.shape[0])
+
+
+def tree_from_gen(tree, payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0) -> PlenOctree:
+    """Upload a ``gen.Tree`` (input-generator output)."""
+    return po_tree_create(tree.child, tree.sigma, tree.sh, tree.depth, tree.sh_degree, tree.bbox_min, tree.edge,
+                          payload, sh_sign, device)
+
+
+def po_render(tree: PlenOctree, cams, W: int, H: int, out=None, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
+              stream=None):
+    """cams: CUDA uint8/float32 tensor holding po_camera records ([n][16] float32). Returns [n][H][W][3]."""
+    import torch
+    cams = _need(cams, torch.float32, (16,))
+    n = cams.shape[0]
+    if out is None:
+        out = torch.empty((n, H, W, 3), dtype=torch.float32, device=cams.device)
+    _need(out, torch.float32, (H, W, 3))
+    o = _opts(gamma, background)
+    _check(lib().po_render(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), _ptr(out), _stream(stream)))
+    return out
+
+
+def po_render_host(tree: PlenOctree, cams_host: np.ndarray, W: int, H: int, out_host=None, gamma: float = 0.01,
+                   background=(1.0, 1.0, 1.0), stream=None):
+    """Host cameras (float32 [n][16]) -> host image (float32 [n][H][W][3], pinned recommended). Synchronous."""
+    cams_host = np.ascontiguousarray(np.asarray(cams_host).view(np.float32).reshape(-1, 16))
+    n = cams_host.shape[0]
+    if out_host is None:
+        out_host = np.empty((n, H, W, 3), np.float32)
+    o = _opts(gamma, background)
+    _check(lib().po_render_host(tree.handle, _ptr(cams_host), n, W, H, ctypes.byref(o), _ptr(out_host),
+                                _stream(stream)))
+    return out_host
+
+
+def po_render_rays(tree: PlenOctree, rays, out=None, aux=None, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
+                   stream=None):
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    n = rays.shape[0]
+    if out is None:
+        out = torch.empty((n, 3), dtype=torch.float32, device=rays.device)
+    _need(out, torch.float32, (3,))
+    if aux is not None:
+        _need(aux, torch.float64, (4,))
+    o = _opts(gamma, background)
+    _check(lib().po_render_rays(tree.handle, _ptr(rays), n, ctypes.byref(o), _ptr(out), _ptr(aux), _stream(stream)))
+    return out
+
+
+def po_render_backward(tree: PlenOctree, rays, dL_dC, grad_sigma, grad_sh, aux=None, gamma: float = 0.0,
+                       background=(1.0, 1.0, 1.0), stream=None):
+    """Accumulates (+=) dL/dsigma~ into grad_sigma [n_leaves] and dL/dk into grad_sh [n_leaves][B][3]."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    _need(dL_dC, torch.float32, (3,))
+    _need(grad_sigma, torch.float32)
+    _need(grad_sh, torch.float32, (tree.B, 3))
+    if aux is not None:
+        _need(aux, torch.float64, (4,))
+    o = _opts(gamma, background)
+    _check(lib().po_render_backward(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux), ctypes.byref(o),
+                                    _ptr(grad_sigma), _ptr(grad_sh), _stream(stream)))
+
+
+def po_l2_loss_grad(pred, target, dL_dC=None, loss=None, stream=None):
+    import torch
+    _need(pred, torch.float32, (3,))
+    _need(target, torch.float32, (3,))
+    if dL_dC is None:
+        dL_dC = torch.empty_like(pred)
+    if loss is not None:
+        _need(loss, torch.float64)
+    _check(lib().po_l2_loss_grad(_ptr(pred), _ptr(target), pred.shape[0], _ptr(dL_dC), _ptr(loss),
+                                 pred.device.index or 0, _stream(stream)))
+    return dL_dC
+
+
+def po_tree_sgd_step(tree: PlenOctree, grad_sigma, grad_sh, lr: float, stream=None):
+    _check(lib().po_tree_sgd_step(tree.handle, _ptr(grad_sigma), _ptr(grad_sh), float(lr), _stream(stream)))
+
+
+def po_trace(tree: PlenOctree, rays, max_leaves: int = 64, gamma: float = 0.01, with_nodes: bool = True,
+             stream=None):
+    """Returns (leaf_ids int32 [n][max_leaves], counts int32 [n], node_counts int32 [n] or None)."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    n = rays.shape[0]
+    dev = rays.device
+    ids = torch.empty((n, max_leaves), dtype=torch.int32, device=dev) if max_leaves > 0 else None
+    counts = torch.empty(n, dtype=torch.int32, device=dev)
+    nodes = torch.empty(n, dtype=torch.int32, device=dev) if with_nodes else None
+    o = _opts(gamma, (1.0, 1.0, 1.0))
+    _check(lib().po_trace(tree.handle, _ptr(rays), n, ctypes.byref(o), max_leaves, _ptr(ids), _ptr(counts),
+                          _ptr(nodes), _stream(stream)))
+    return ids, counts, nodes
+
+
+def po_render_stats(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.01, stream=None):
+    """Returns dict(leaf_visits, sh_rows, nodes, hit_rays) for one po_render over ``cams``."""
+    import torch
+    cams = _need(cams, torch.float32, (16,))
+    ctr = torch.zeros(4, dtype=torch.int64, device=cams.device)
+    o = _opts(gamma, (1.0, 1.0, 1.0))
+    _check(lib().po_render_stats(tree.handle, _ptr(cams), cams.shape[0], W, H, ctypes.byref(o), _ptr(ctr),
+                                 _stream(stream)))
+    v = ctr.cpu().tolist()
+    return dict(leaf_visits=v[0], sh_rows=v[1], nodes=v[2], hit_rays=v[3])
+
+
+def launch_count() -> int:
+    return int(lib().po_launch_count())
+
+
+def cams_tensor(cam_records, device="cuda"):
+    """po_camera records (numpy structured or float32 [n][16]) -> CUDA float32 [n][16]."""
+    import torch
+    a = np.ascontiguousarray(cam_records)
+    a = np.frombuffer(a.tobytes(), dtype=np.float32).reshape(-1, 16).copy()
+    return torch.from_numpy(a).to(device)

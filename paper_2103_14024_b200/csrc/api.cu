@@ -1,0 +1,433 @@
+// C-ABI layer of libplenoct (include/plenoct.h): argument validation, tree upload (a0),
+// device selection and kernel launches.  No compute happens here; there is no CPU path.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "plenoct.h"
+
+struct po_tree {
+    po_tree_desc desc;
+    int64_t n_nodes = 0, n_leaves = 0;
+    int B = 0, ne = 0;          // basis size, 3B elements per leaf
+    int sh_row = 0;             // padded row in elements
+    int sh_row_bytes = 0;
+    uint32_t* d_child = nullptr;
+    float* d_sigma = nullptr;
+    void* d_sh = nullptr;
+    po_camera* d_cams = nullptr;   // scratch for po_render_host
+    int cam_cap = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+po_status fail(po_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+po_status fail(po_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+po_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return PO_OK;
+    if (e == cudaErrorMemoryAllocation) return fail(PO_ERR_OOM, "%s: %s", where, cudaGetErrorString(e));
+    return fail(PO_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+// Switches the calling thread to the tree's device for the duration of a call.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+po::DevTree dev_tree(const po_tree* t) {
+    po::DevTree d;
+    d.child = t->d_child;
+    d.sigma = t->d_sigma;
+    d.sh = t->d_sh;
+    d.sh_row = t->sh_row;
+    d.depth = t->desc.max_depth;
+    for (int k = 0; k < 3; ++k) d.bmin[k] = t->desc.bbox_min[k];
+    d.scale = (float)std::ldexp(1.0, t->desc.max_depth) / t->desc.bbox_edge;
+    d.odd_sign = t->desc.sh_sign == PO_SH_NO_CS ? -1.f : 1.f;
+    return d;
+}
+
+po_status check_opts(const po_render_opts* o, po::RenderOpts* out) {
+    if (!o) return fail(PO_ERR_INVALID_ARG, "opts is NULL");
+    if (!(o->gamma >= 0.f && o->gamma <= 1.f)) return fail(PO_ERR_INVALID_ARG, "gamma %g outside [0,1]", o->gamma);
+    out->gamma = o->gamma;
+    for (int k = 0; k < 3; ++k) {
+        if (!std::isfinite(o->background[k])) return fail(PO_ERR_INVALID_ARG, "background[%d] not finite", k);
+        out->bg[k] = o->background[k];
+    }
+    return PO_OK;
+}
+
+po_status check_tree(const po_tree* t) {
+    if (!t || !t->d_child) return fail(PO_ERR_INVALID_ARG, "tree is NULL or destroyed");
+    return PO_OK;
+}
+
+po_status launched(cudaError_t e, const char* where) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_status(e, where);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* po_last_error(void) { return g_err.c_str(); }
+const char* po_version(void) { return "libplenoct 0.1 sm_100a"; }
+int64_t po_launch_count(void) { return g_launches.load(); }
+
+po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_t n_nodes, const float* sigma,
+                         const float* sh, int64_t n_leaves, po_tree** out) {
+    if (!out) return fail(PO_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!desc) return fail(PO_ERR_INVALID_ARG, "desc is NULL");
+    if (!(desc->bbox_edge > 0.f) || !std::isfinite(desc->bbox_edge))
+        return fail(PO_ERR_INVALID_ARG, "bbox_edge must be finite and > 0");
+    for (int k = 0; k < 3; ++k)
+        if (!std::isfinite(desc->bbox_min[k])) return fail(PO_ERR_INVALID_ARG, "bbox_min[%d] not finite", k);
+    if (desc->max_depth < 1 || desc->max_depth > po::kMaxDepth)
+        return fail(PO_ERR_INVALID_ARG, "max_depth %d outside [1,%d]", desc->max_depth, po::kMaxDepth);
+    if (desc->sh_degree < 0 || desc->sh_degree > 3)
+        return fail(PO_ERR_UNSUPPORTED, "sh_degree %d unsupported (0..3)", desc->sh_degree);
+    if (desc->payload != PO_F32 && desc->payload != PO_F16)
+        return fail(PO_ERR_UNSUPPORTED, "payload %d unsupported", desc->payload);
+    if (desc->sh_sign != PO_SH_CS && desc->sh_sign != PO_SH_NO_CS)
+        return fail(PO_ERR_INVALID_ARG, "sh_sign %d invalid", desc->sh_sign);
+    if (n_nodes < 1 || !child) return fail(PO_ERR_INVALID_ARG, "need n_nodes >= 1 and a child table");
+    if (n_leaves < 0 || n_leaves > (int64_t)po::kIdxMask + 1 || n_nodes > (int64_t)po::kIdxMask + 1)
+        return fail(PO_ERR_INVALID_ARG, "n_leaves / n_nodes out of range");
+    if (n_leaves > 0 && (!sigma || !sh)) return fail(PO_ERR_INVALID_ARG, "sigma / sh NULL with n_leaves > 0");
+
+    // ---- structural validation: BFS from the root with levels ----
+    const int D = desc->max_depth;
+    std::vector<int8_t> node_level((size_t)n_nodes, -1);
+    std::vector<uint8_t> leaf_seen((size_t)n_leaves, 0);
+    std::vector<int64_t> queue;
+    queue.reserve((size_t)n_nodes);
+    queue.push_back(0);
+    node_level[0] = 0;
+    for (size_t qi = 0; qi < queue.size(); ++qi) {
+        const int64_t nd = queue[qi];
+        const int L = node_level[(size_t)nd];
+        for (int o = 0; o < 8; ++o) {
+            const uint32_t e = child[nd * 8 + o];
+            const uint32_t tag = e >> 30, idx = e & po::kIdxMask;
+            if (tag == po::kTagEmpty) continue;
+            if (tag == po::kTagInternal) {
+                if ((int64_t)idx >= n_nodes)
+                    return fail(PO_ERR_INVALID_TREE, "node %lld slot %d: child node %u out of range", (long long)nd, o, idx);
+                if (L + 1 >= D)
+                    return fail(PO_ERR_INVALID_TREE, "node %lld slot %d: internal node at level %d >= max_depth", (long long)nd, o, L + 1);
+                if (node_level[idx] >= 0 || idx == 0)
+                    return fail(PO_ERR_INVALID_TREE, "node %u referenced twice", idx);
+                node_level[idx] = (int8_t)(L + 1);
+                queue.push_back(idx);
+            } else if (tag == po::kTagLeaf) {
+                if ((int64_t)idx >= n_leaves)
+                    return fail(PO_ERR_INVALID_TREE, "node %lld slot %d: leaf %u out of range", (long long)nd, o, idx);
+                if (leaf_seen[idx]) return fail(PO_ERR_INVALID_TREE, "leaf %u referenced twice", idx);
+                leaf_seen[idx] = 1;
+            } else {
+                return fail(PO_ERR_INVALID_TREE, "node %lld slot %d: bad tag 3", (long long)nd, o);
+            }
+        }
+    }
+    if ((int64_t)queue.size() != n_nodes)
+        return fail(PO_ERR_INVALID_TREE, "%lld of %lld nodes unreachable from the root",
+                    (long long)(n_nodes - (int64_t)queue.size()), (long long)n_nodes);
+    const int B = (desc->sh_degree + 1) * (desc->sh_degree + 1);
+    const int ne = 3 * B;
+    for (int64_t i = 0; i < n_leaves; ++i) {
+        if (!std::isfinite(sigma[i])) return fail(PO_ERR_INVALID_TREE, "sigma of leaf %lld not finite", (long long)i);
+        for (int j = 0; j < ne; ++j)
+            if (!std::isfinite(sh[i * ne + j]))
+                return fail(PO_ERR_INVALID_TREE, "sh of leaf %lld element %d not finite", (long long)i, j);
+    }
+
+    // ---- device layout: child table as is; sigma~ SoA; SH rows padded to 16 B ----
+    const bool f16 = desc->payload == PO_F16;
+    const int per16 = f16 ? 8 : 4;
+    const int row = (ne + per16 - 1) / per16 * per16;
+    const size_t elt = f16 ? 2 : 4;
+    DeviceGuard g(desc->device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    po_tree* t = new po_tree();
+    t->desc = *desc;
+    t->n_nodes = n_nodes;
+    t->n_leaves = n_leaves;
+    t->B = B;
+    t->ne = ne;
+    t->sh_row = row;
+    t->sh_row_bytes = (int)(row * elt);
+    auto cleanup = [&](po_status s) {
+        po_tree_destroy(t);
+        return s;
+    };
+    cudaError_t e = cudaMalloc(&t->d_child, (size_t)n_nodes * 8 * sizeof(uint32_t));
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(child)"));
+    e = cudaMalloc(&t->d_sigma, (size_t)std::max<int64_t>(n_leaves, 1) * sizeof(float));
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sigma)"));
+    e = cudaMalloc(&t->d_sh, (size_t)std::max<int64_t>(n_leaves, 1) * row * elt);
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
+    e = cudaMemcpy(t->d_child, child, (size_t)n_nodes * 8 * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "upload child"));
+    if (n_leaves > 0) {
+        e = cudaMemcpy(t->d_sigma, sigma, (size_t)n_leaves * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cleanup(cuda_status(e, "upload sigma"));
+        // pack rows in chunks through a host staging buffer
+        const int64_t chunk = 1 << 16;
+        std::vector<uint8_t> stage((size_t)chunk * row * elt);
+        for (int64_t s0 = 0; s0 < n_leaves; s0 += chunk) {
+            const int64_t nn = std::min(chunk, n_leaves - s0);
+            std::memset(stage.data(), 0, stage.size());
+            for (int64_t i = 0; i < nn; ++i) {
+                const float* src = sh + (s0 + i) * ne;
+                if (f16) {
+                    __half* dst = reinterpret_cast<__half*>(stage.data()) + i * row;
+                    for (int j = 0; j < ne; ++j) dst[j] = __float2half_rn(src[j]);
+                } else {
+                    float* dst = reinterpret_cast<float*>(stage.data()) + i * row;
+                    std::memcpy(dst, src, ne * sizeof(float));
+                }
+            }
+            e = cudaMemcpy(static_cast<uint8_t*>(t->d_sh) + (size_t)s0 * row * elt, stage.data(), (size_t)nn * row * elt,
+                           cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cleanup(cuda_status(e, "upload sh"));
+        }
+    }
+    *out = t;
+    return PO_OK;
+}
+
+po_status po_tree_destroy(po_tree* t) {
+    if (!t) return PO_OK;
+    DeviceGuard g(t->desc.device);
+    if (t->d_child) cudaFree(t->d_child);
+    if (t->d_sigma) cudaFree(t->d_sigma);
+    if (t->d_sh) cudaFree(t->d_sh);
+    if (t->d_cams) cudaFree(t->d_cams);
+    t->d_child = nullptr;
+    delete t;
+    return PO_OK;
+}
+
+po_status po_tree_info(const po_tree* t, int64_t* n_nodes, int64_t* n_leaves, int32_t* sh_row_bytes) {
+    if (po_status s = check_tree(t)) return s;
+    if (n_nodes) *n_nodes = t->n_nodes;
+    if (n_leaves) *n_leaves = t->n_leaves;
+    if (sh_row_bytes) *sh_row_bytes = t->sh_row_bytes;
+    return PO_OK;
+}
+
+po_status po_tree_read_leaves(const po_tree* t, float* sigma, float* sh) {
+    if (po_status s = check_tree(t)) return s;
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e, "sync");
+    if (t->n_leaves == 0) return PO_OK;
+    if (sigma) {
+        e = cudaMemcpy(sigma, t->d_sigma, (size_t)t->n_leaves * sizeof(float), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_status(e, "read sigma");
+    }
+    if (sh) {
+        const bool f16 = t->desc.payload == PO_F16;
+        const size_t elt = f16 ? 2 : 4;
+        std::vector<uint8_t> buf((size_t)t->n_leaves * t->sh_row * elt);
+        e = cudaMemcpy(buf.data(), t->d_sh, buf.size(), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_status(e, "read sh");
+        for (int64_t i = 0; i < t->n_leaves; ++i)
+            for (int j = 0; j < t->ne; ++j)
+                sh[i * t->ne + j] = f16 ? __half2float(reinterpret_cast<const __half*>(buf.data())[i * t->sh_row + j])
+                                        : reinterpret_cast<const float*>(buf.data())[i * t->sh_row + j];
+    }
+    return PO_OK;
+}
+
+static po_status check_image(int32_t n_cams, int32_t W, int32_t H) {
+    if (n_cams < 0 || W <= 0 || H <= 0) return fail(PO_ERR_INVALID_ARG, "need n_cams >= 0, W > 0, H > 0");
+    if (n_cams > 65535) return fail(PO_ERR_INVALID_ARG, "n_cams > 65535 per call");
+    return PO_OK;
+}
+
+static po_status check_cams_host(const po_camera* c, int32_t n) {
+    for (int i = 0; i < n; ++i) {
+        if (!(c[i].fx > 0.f) || !(c[i].fy > 0.f)) return fail(PO_ERR_INVALID_ARG, "camera %d: focal <= 0", i);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                double dot = 0.0;
+                for (int k = 0; k < 3; ++k) dot += (double)c[i].c2w[k][a] * c[i].c2w[k][b];
+                if (std::fabs(dot - (a == b ? 1.0 : 0.0)) > 1e-4)
+                    return fail(PO_ERR_INVALID_ARG, "camera %d: rotation not orthonormal", i);
+            }
+    }
+    return PO_OK;
+}
+
+po_status po_render(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                    const po_render_opts* opts, float* out_rgb, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    if (po_status s = check_image(n_cams, W, H)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n_cams == 0) return PO_OK;
+    if (!cams || !out_rgb) return fail(PO_ERR_INVALID_ARG, "cams / out_rgb NULL");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
+                                      out_rgb, (cudaStream_t)stream),
+                    "po_render");
+}
+
+po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
+                         const po_render_opts* opts, float* out_host, po_stream stream) {
+    po_tree* t = const_cast<po_tree*>(tc);   // only the camera scratch is mutated
+    if (po_status s = check_tree(t)) return s;
+    if (po_status s = check_image(n_cams, W, H)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n_cams == 0) return PO_OK;
+    if (!cams_host || !out_host) return fail(PO_ERR_INVALID_ARG, "cams / out NULL");
+    if (po_status s = check_cams_host(cams_host, n_cams)) return s;
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (t->cam_cap < n_cams) {
+        if (t->d_cams) cudaFree(t->d_cams);
+        t->d_cams = nullptr;
+        t->cam_cap = 0;
+        cudaError_t e = cudaMalloc(&t->d_cams, sizeof(po_camera) * (size_t)n_cams);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(cams)");
+        t->cam_cap = n_cams;
+    }
+    cudaError_t e = cudaMemcpyAsync(t->d_cams, cams_host, sizeof(po_camera) * (size_t)n_cams, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "H2D cams");
+    float* d_out = nullptr;
+    const size_t out_bytes = (size_t)n_cams * W * H * 3 * sizeof(float);
+    e = cudaMallocAsync((void**)&d_out, out_bytes, s);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(out)");
+    po_status st = launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, t->d_cams,
+                                              n_cams, W, H, o, d_out, s),
+                            "po_render_host");
+    if (st == PO_OK) {
+        e = cudaMemcpyAsync(out_host, d_out, out_bytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = cuda_status(e, "D2H image");
+    }
+    cudaFreeAsync(d_out, s);
+    e = cudaStreamSynchronize(s);
+    if (st == PO_OK && e != cudaSuccess) st = cuda_status(e, "sync");
+    return st;
+}
+
+po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, float* out_rgb,
+                         double* aux, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (n == 0) return PO_OK;
+    if (!rays || !out_rgb) return fail(PO_ERR_INVALID_ARG, "rays / out_rgb NULL");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_render_rays(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, o,
+                                           out_rgb, aux, (cudaStream_t)stream),
+                    "po_render_rays");
+}
+
+po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, const float* dL_dC, const double* aux,
+                             const po_render_opts* opts, float* grad_sigma, float* grad_sh, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (n == 0) return PO_OK;
+    if (!rays || !dL_dC || !grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
+                                        o, grad_sigma, grad_sh, (cudaStream_t)stream),
+                    "po_render_backward");
+}
+
+po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, float* dL_dC, double* loss,
+                          int32_t device, po_stream stream) {
+    if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (n > 0 && (!pred || !target || !dL_dC)) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_l2_loss(pred, target, n * 3, dL_dC, loss, (cudaStream_t)stream), "po_l2_loss_grad");
+}
+
+po_status po_tree_sgd_step(po_tree* t, const float* grad_sigma, const float* grad_sh, float lr, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    if (t->desc.payload != PO_F32) return fail(PO_ERR_UNSUPPORTED, "SGD needs an fp32 payload (P:973 trains in fp32)");
+    if (!std::isfinite(lr)) return fail(PO_ERR_INVALID_ARG, "lr not finite");
+    if (t->n_leaves == 0) return PO_OK;
+    if (!grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL gradient");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_sgd(t->d_sigma, static_cast<float*>(t->d_sh), t->sh_row, t->ne, t->n_leaves, grad_sigma,
+                                   grad_sh, lr, (cudaStream_t)stream),
+                    "po_tree_sgd_step");
+}
+
+po_status po_trace(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, int32_t max_leaves,
+                   int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n < 0 || max_leaves < 0) return fail(PO_ERR_INVALID_ARG, "n < 0 or max_leaves < 0");
+    if (n == 0) return PO_OK;
+    if (!rays || (max_leaves > 0 && !leaf_ids)) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_trace(dev_tree(t), rays, n, o.gamma, max_leaves, max_leaves > 0 ? leaf_ids : nullptr,
+                                     counts, node_counts, (cudaStream_t)stream),
+                    "po_trace");
+}
+
+po_status po_render_stats(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                          const po_render_opts* opts, unsigned long long* counters, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    if (po_status s = check_image(n_cams, W, H)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n_cams == 0) return PO_OK;
+    if (!cams || !counters) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_stats(dev_tree(t), cams, n_cams, W, H, o.gamma, counters, (cudaStream_t)stream),
+                    "po_render_stats");
+}
+
+}  // extern "C"

@@ -1,0 +1,441 @@
+// CUDA kernels of the PlenOctree hot path for sm_100a.
+//
+//   k_render        a1..a6   one thread per pixel, warp = 8x4 pixel tile, CTA = 16x16
+//   k_render_rays   a2..a6   one thread per ray (optionally double-precision totals, aux)
+//   k_backward      a7+a8    two passes per ray in ONE thread: pass 1 (or aux)
+//                            gives the total sum_k c_k w_k, pass 2 re-traverses with a
+//                            double prefix and scatter-adds per-leaf gradients
+//   k_trace/k_stats          parity / measurement visitors over the same traversal
+//   k_l2_loss, k_sgd         Eq. (3) gradient helper and the SGD update
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "traverse.cuh"
+
+namespace po {
+
+// ---------------------------------------------------------------------------------------
+// Visitors
+// ---------------------------------------------------------------------------------------
+template <int DEG, bool F16>
+struct FwdVisitor {
+    const DevTree& tr;
+    float Y[ShDim<DEG>::B];
+    float T, gamma;
+    float C[3];
+    __device__ FwdVisitor(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g) {
+        sh_basis<DEG>(d, t.odd_sign, Y);
+        C[0] = C[1] = C[2] = 0.f;
+    }
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;   // sigma = (sigma~)_+ = 0: alpha = 0 (reading Q10)
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+        float z[3];
+        sh_dot<DEG, F16>(tr, idx, Y, z);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(a.w, sigmoidf_(z[ch]), C[ch]);
+        T = a.Tn;
+        return !(T < gamma);
+    }
+};
+
+// Forward with the colour sum accumulated in double (pass 1 of the backward).
+template <int DEG, bool F16>
+struct TotalVisitor {
+    const DevTree& tr;
+    float Y[ShDim<DEG>::B];
+    float T, gamma;
+    double C[3];
+    __device__ TotalVisitor(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g) {
+        sh_basis<DEG>(d, t.odd_sign, Y);
+        C[0] = C[1] = C[2] = 0.0;
+    }
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+        float z[3];
+        sh_dot<DEG, F16>(tr, idx, Y, z);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) C[ch] += (double)a.w * (double)sigmoidf_(z[ch]);
+        T = a.Tn;
+        return !(T < gamma);
+    }
+};
+
+// Pass 2: prefix P_i = sum_{k<=i} c_k w_k (double); S_i = total - P_i;
+// dL/dsigma~_i = [sigma~_i > 0] delta_i sum_ch g_ch (c_i,ch T_{i+1} - S_i,ch)
+// dL/dk_i,b,ch = g_ch w_i c_i,ch (1 - c_i,ch) Y_b
+template <int DEG, bool F16>
+struct GradVisitor {
+    const DevTree& tr;
+    float Y[ShDim<DEG>::B];
+    float T, gamma;
+    double P[3], Ctot[3];
+    float g[3];
+    float* __restrict__ grad_sigma;
+    float* __restrict__ grad_sh;
+    __device__ GradVisitor(const DevTree& t, const float d[3], float gm, float* gs, float* gk)
+        : tr(t), T(1.f), gamma(gm), grad_sigma(gs), grad_sh(gk) {
+        sh_basis<DEG>(d, t.odd_sign, Y);
+        P[0] = P[1] = P[2] = 0.0;
+    }
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;   // ReLU gate: w = 0 and dsigma = 0
+        const float delta = __fsub_rn(t1, t0);
+        const Absorb a = absorb(T, st, delta);
+        float z[3], c[3];
+        sh_dot<DEG, F16>(tr, idx, Y, z);
+        double acc = 0.0;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            c[ch] = sigmoidf_(z[ch]);
+            P[ch] += (double)a.w * (double)c[ch];
+            acc += (double)g[ch] * ((double)c[ch] * (double)a.Tn - (Ctot[ch] - P[ch]));
+        }
+        atomicAdd(grad_sigma + idx, (float)((double)delta * acc));
+        constexpr int B = ShDim<DEG>::B;
+        constexpr int NE = 3 * B;
+        float gz[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gz[ch] = g[ch] * a.w * c[ch] * (1.f - c[ch]);
+        float* row = grad_sh + (size_t)idx * NE;
+        if constexpr (NE % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < NE / 4; ++j) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3];
+                float* p = row + 4 * j;
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                             "f"(v[2]), "f"(v[3])
+                             : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int el = 0; el < NE; ++el) atomicAdd(row + el, gz[el % 3] * Y[el / 3]);
+        }
+        T = a.Tn;
+        return !(T < gamma);
+    }
+};
+
+struct TraceVisitor {
+    const DevTree& tr;
+    float T, gamma;
+    int32_t* ids;
+    int32_t max_leaves, count, nodes;
+    __device__ __forceinline__ void on_node() { ++nodes; }
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        if (count < max_leaves) ids[count] = (int32_t)idx;
+        ++count;
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;
+        T = absorb(T, st, __fsub_rn(t1, t0)).Tn;
+        return !(T < gamma);
+    }
+};
+
+struct StatsVisitor {
+    const DevTree& tr;
+    float T, gamma;
+    unsigned long long leaves, sh_rows, nodes;
+    __device__ __forceinline__ void on_node() { ++nodes; }
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        ++leaves;
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;
+        ++sh_rows;
+        T = absorb(T, st, __fsub_rn(t1, t0)).Tn;
+        return !(T < gamma);
+    }
+};
+
+// ---------------------------------------------------------------------------------------
+// a1: pixel -> ray (reading Q5)
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void camera_ray(const po_camera* __restrict__ cams, int view, int px, int py, float o[3],
+                                           float d[3]) {
+    const float* cm = reinterpret_cast<const float*>(cams + view);
+    float c[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = __ldg(cm + k);
+    const float dx = ((float)px + 0.5f - c[14]) / c[12];
+    const float dy = -((float)py + 0.5f - c[15]) / c[13];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        d[k] = c[k * 4 + 0] * dx + c[k * 4 + 1] * dy - c[k * 4 + 2];
+        o[k] = c[k * 4 + 3];
+    }
+}
+
+// CTA = 16x16 pixels = 8 warps, each warp an 8x4 pixel tile (warp-coherent ray packets).
+__device__ __forceinline__ bool tile_pixel(int W, int H, int& px, int& py) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    px = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
+    py = blockIdx.y * 16 + (warp >> 1) * 4 + (lane >> 3);
+    return px < W && py < H;
+}
+
+template <int DEG, bool F16>
+__global__ void __launch_bounds__(256) k_render(DevTree tr, const po_camera* __restrict__ cams, int W, int H,
+                                                RenderOpts opt, float* __restrict__ out) {
+    int px, py;
+    if (!tile_pixel(W, H, px, py)) return;
+    const int view = blockIdx.z;
+    float o[3], d[3];
+    camera_ray(cams, view, px, py, o, d);
+    RayState r;
+    float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
+    if (ray_setup(tr, o, d, r)) {
+        FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
+        traverse(tr, r, v);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+    }
+    float* p = out + (((size_t)view * H + py) * W + px) * 3;
+    p[0] = C[0];
+    p[1] = C[1];
+    p[2] = C[2];
+}
+
+template <int DEG, bool F16>
+__global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                     RenderOpts opt, float* __restrict__ out, double* __restrict__ aux) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __ldg(rays + i * 6 + k);
+        d[k] = __ldg(rays + i * 6 + 3 + k);
+    }
+    RayState r;
+    const bool hit = ray_setup(tr, o, d, r);
+    if (aux == nullptr) {
+        float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
+        if (hit) {
+            FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
+            traverse(tr, r, v);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+        }
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) out[i * 3 + ch] = C[ch];
+    } else {
+        double C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
+        float T = 1.f;
+        if (hit) {
+            TotalVisitor<DEG, F16> v(tr, r.d, opt.gamma);
+            traverse(tr, r, v);
+            T = v.T;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) C[ch] = v.C[ch] + (double)v.T * (double)opt.bg[ch];
+        }
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            out[i * 3 + ch] = (float)C[ch];
+            aux[i * 4 + ch] = C[ch];
+        }
+        aux[i * 4 + 3] = (double)T;
+    }
+}
+
+template <int DEG, bool F16>
+__global__ void __launch_bounds__(256) k_backward(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                  const float* __restrict__ dL_dC, const double* __restrict__ aux,
+                                                  RenderOpts opt, float* __restrict__ grad_sigma,
+                                                  float* __restrict__ grad_sh) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __ldg(rays + i * 6 + k);
+        d[k] = __ldg(rays + i * 6 + 3 + k);
+    }
+    RayState r;
+    if (!ray_setup(tr, o, d, r)) return;   // a miss touches no leaf
+    GradVisitor<DEG, F16> gv(tr, r.d, opt.gamma, grad_sigma, grad_sh);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) gv.g[ch] = __ldg(dL_dC + i * 3 + ch);
+    if (gv.g[0] == 0.f && gv.g[1] == 0.f && gv.g[2] == 0.f) return;
+    if (aux != nullptr) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = aux[i * 4 + ch];
+    } else {   // pass 1: total = sum_{k<=N} c_k w_k including the background
+        TotalVisitor<DEG, F16> tv(tr, r.d, opt.gamma);
+        traverse(tr, r, tv);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = tv.C[ch] + (double)tv.T * (double)opt.bg[ch];
+    }
+    traverse(tr, r, gv);
+}
+
+__global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restrict__ rays, int64_t n, float gamma,
+                                               int32_t max_leaves, int32_t* __restrict__ leaf_ids,
+                                               int32_t* __restrict__ counts, int32_t* __restrict__ node_counts) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = rays[i * 6 + k];
+        d[k] = rays[i * 6 + 3 + k];
+    }
+    int32_t* ids = leaf_ids ? leaf_ids + i * max_leaves : nullptr;
+    for (int j = 0; j < max_leaves && ids; ++j) ids[j] = -1;
+    TraceVisitor v{tr, 1.f, gamma, ids, ids ? max_leaves : 0, 0, 0};
+    RayState r;
+    if (ray_setup(tr, o, d, r)) traverse(tr, r, v);
+    if (counts) counts[i] = v.count;
+    if (node_counts) node_counts[i] = v.nodes;
+}
+
+__global__ void __launch_bounds__(256) k_stats(DevTree tr, const po_camera* __restrict__ cams, int W, int H,
+                                               float gamma, unsigned long long* __restrict__ counters) {
+    int px, py;
+    unsigned long long v4[4] = {0, 0, 0, 0};
+    if (tile_pixel(W, H, px, py)) {
+        float o[3], d[3];
+        camera_ray(cams, blockIdx.z, px, py, o, d);
+        RayState r;
+        if (ray_setup(tr, o, d, r)) {
+            StatsVisitor v{tr, 1.f, gamma, 0, 0, 0};
+            traverse(tr, r, v);
+            v4[0] = v.leaves;
+            v4[1] = v.sh_rows;
+            v4[2] = v.nodes;
+            v4[3] = 1;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        unsigned long long s = v4[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(counters + k, s);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_l2_loss(const float* __restrict__ pred, const float* __restrict__ target,
+                                                 int64_t n3, float* __restrict__ dL_dC, double* __restrict__ loss) {
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += (int64_t)gridDim.x * blockDim.x) {
+        const float diff = pred[i] - target[i];
+        dL_dC[i] = 2.0f * diff;
+        acc += (double)diff * (double)diff;
+    }
+    if (loss == nullptr) return;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        atomicAdd(loss, s);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* __restrict__ sh, int32_t sh_row,
+                                             int32_t ne, int64_t n_leaves, const float* __restrict__ grad_sigma,
+                                             const float* __restrict__ grad_sh, float lr) {
+    const int64_t total = n_leaves * (int64_t)(ne + 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n_leaves) {
+            sigma[i] -= lr * grad_sigma[i];
+        } else {
+            const int64_t j = i - n_leaves;
+            const int64_t leaf = j / ne;
+            const int64_t el = j - leaf * ne;
+            sh[leaf * sh_row + el] -= lr * grad_sh[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Launchers (dispatch on SH degree x payload)
+// ---------------------------------------------------------------------------------------
+#define PO_DISPATCH(DEGV, F16V, ...)                                   \
+    switch ((DEGV) * 2 + ((F16V) ? 1 : 0)) {                           \
+        case 0: { constexpr int DEG = 0; constexpr bool F16 = false; __VA_ARGS__; } break; \
+        case 1: { constexpr int DEG = 0; constexpr bool F16 = true; __VA_ARGS__; } break;  \
+        case 2: { constexpr int DEG = 1; constexpr bool F16 = false; __VA_ARGS__; } break; \
+        case 3: { constexpr int DEG = 1; constexpr bool F16 = true; __VA_ARGS__; } break;  \
+        case 4: { constexpr int DEG = 2; constexpr bool F16 = false; __VA_ARGS__; } break; \
+        case 5: { constexpr int DEG = 2; constexpr bool F16 = true; __VA_ARGS__; } break;  \
+        case 6: { constexpr int DEG = 3; constexpr bool F16 = false; __VA_ARGS__; } break; \
+        case 7: { constexpr int DEG = 3; constexpr bool F16 = true; __VA_ARGS__; } break;  \
+        default: return cudaErrorInvalidValue;                         \
+    }
+
+static inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
+                          const RenderOpts& opt, float* out, cudaStream_t s) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, n_cams);
+    PO_DISPATCH(deg, f16, k_render<DEG, F16><<<grid, 256, 0, s>>>(tr, cams, W, H, opt, out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
+                               const RenderOpts& opt, float* out, double* aux, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    PO_DISPATCH(deg, f16, k_render_rays<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out, aux));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
+                            const double* aux, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
+                            cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    PO_DISPATCH(deg, f16,
+                k_backward<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, opt, grad_sigma, grad_sh));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
+                         int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_trace<<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, max_leaves, leaf_ids, counts, node_counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, int W, int H, float gamma,
+                         unsigned long long* counters, cudaStream_t s) {
+    dim3 grid((W + 15) / 16, (H + 15) / 16, n_cams);
+    k_stats<<<grid, 256, 0, s>>>(tr, cams, W, H, gamma, counters);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, float* dL_dC, double* loss,
+                           cudaStream_t s) {
+    if (loss) {
+        cudaError_t e = cudaMemsetAsync(loss, 0, sizeof(double), s);
+        if (e != cudaSuccess) return e;
+    }
+    if (n3 == 0) return cudaSuccess;
+    unsigned g = grid1d(n3, 256);
+    if (g > 148 * 16) g = 148 * 16;
+    k_l2_loss<<<g, 256, 0, s>>>(pred, target, n3, dL_dC, loss);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, const float* grad_sigma,
+                       const float* grad_sh, float lr, cudaStream_t s) {
+    const int64_t total = n_leaves * (int64_t)(ne + 1);
+    if (total == 0) return cudaSuccess;
+    unsigned g = grid1d(total, 256);
+    if (g > 148 * 32) g = 148 * 32;
+    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr);
+    return cudaGetLastError();
+}
+
+}  // namespace po

@@ -1,0 +1,32 @@
+// Internal launcher interface between the C-ABI layer (api.cu) and the kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "plenoct.h"
+#include "traverse.cuh"
+
+namespace po {
+
+struct RenderOpts {
+    float gamma;
+    float bg[3];
+};
+
+cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
+                          const RenderOpts& opt, float* out, cudaStream_t s);
+cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
+                               const RenderOpts& opt, float* out, double* aux, cudaStream_t s);
+cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
+                            const double* aux, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
+                            cudaStream_t s);
+cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
+                         int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s);
+cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, int W, int H, float gamma,
+                         unsigned long long* counters, cudaStream_t s);
+cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, float* dL_dC, double* loss,
+                           cudaStream_t s);
+cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, const float* grad_sigma,
+                       const float* grad_sh, float lr, cudaStream_t s);
+
+}  // namespace po

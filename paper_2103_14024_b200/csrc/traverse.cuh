@@ -1,0 +1,247 @@
+// Device-side building blocks of the PlenOctree hot path (sm_100a).
+//
+//   ray setup + AABB clip ......... SURVEY §8(a) a1/a2, reading Q5/Q6
+//   ordered octree descent ........ a3, PAPER P:424-433 ("skipping large voxels in one step
+//                                   while also not missing small voxels")
+//   SH basis, colour .............. a5, P:296-300 (Eq. 5), P:749-767 (App. B.1)
+//   alpha / transmittance ......... a4/a6, P:238-243 (Eq. 1-2), P:435-437 (early stop)
+//
+// Traversal design (B200-first, not the paper's): the ray lives in integer leaf-grid
+// coordinates (the cube is [0, 2^D)^3, leaf cells are unit cubes).  Every plane crossing
+// is computed from scratch as t = (plane - o') * inv with an exactly representable
+// integer plane, and consecutive segments share their boundary t.  The current cell
+// is a triple of integers; after leaving a box through face `ax`, the neighbour cell is
+// known exactly on that axis and by point location on the other two (clamped to the
+// box).  The descent restarts at the deepest common ancestor, found with one clz of
+// (old XOR new) cell coordinates, from a per-thread ancestor stack.  Empty coarse boxes
+// are skipped in one step.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace po {
+
+constexpr uint32_t kTagEmpty = 0u, kTagInternal = 1u, kTagLeaf = 2u;
+constexpr uint32_t kIdxMask = (1u << 30) - 1u;
+constexpr int kMaxDepth = 15;
+
+struct DevTree {
+    const uint32_t* __restrict__ child;   // [n_nodes][8]
+    const float* __restrict__ sigma;      // [n_leaves]   sigma~
+    const void* __restrict__ sh;          // [n_leaves][row] fp32 or fp16, rows 16-B aligned
+    int32_t sh_row;                       // row stride in elements
+    int32_t depth;
+    float bmin[3];
+    float scale;                          // 2^D / edge
+    float odd_sign;                       // +1 (Condon-Shortley reading) or -1
+};
+
+struct RayState {
+    float o[3];     // origin in grid units
+    float dg[3];    // unit direction * scale (grid units per world unit)
+    float inv[3];   // 1 / dg (world t per grid unit), +inf for a zero component
+    float d[3];     // unit world direction (SH argument, reading Q15)
+    float tnear, tfar;
+};
+
+// a1/a2: normalise d, move to grid units, slab-clip against [0, 2^D]^3.
+__device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], const float dir[3], RayState& r) {
+    float n2 = dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2];
+    if (!(n2 > 0.f) || !(n2 < INFINITY)) return false;
+    float rn = 1.0f / sqrtf(n2);
+    const float G = (float)(1 << tr.depth);
+    float tn = 0.f, tf = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        r.d[k] = dir[k] * rn;
+        r.o[k] = (o[k] - tr.bmin[k]) * tr.scale;
+        r.dg[k] = r.d[k] * tr.scale;
+        if (r.dg[k] != 0.f) {
+            r.inv[k] = 1.0f / r.dg[k];
+            float ta = (0.f - r.o[k]) * r.inv[k];
+            float tb = (G - r.o[k]) * r.inv[k];
+            tn = fmaxf(tn, fminf(ta, tb));
+            tf = fminf(tf, fmaxf(ta, tb));
+        } else {
+            r.inv[k] = INFINITY;
+            if (!(r.o[k] >= 0.f && r.o[k] <= G)) return false;
+        }
+    }
+    r.tnear = tn;
+    r.tfar = tf;
+    return tf > tn;
+}
+
+// Cell index on one axis of the point o' + t*dg, for a ray moving with slope dg:
+// the cell the ray is about to traverse (ceil-1 when moving down).
+__device__ __forceinline__ int cell_of(float o, float dg, float t) {
+    float p = fmaf(t, dg, o);
+    return dg < 0.f ? (int)ceilf(p) - 1 : (int)floorf(p);
+}
+
+// a3: ordered descent.  Calls vis.on_node() for every internal node entered (root
+// included) and vis.on_leaf(idx, t_in, t_out) for every positive-length leaf segment in
+// ray order; traversal stops when on_leaf returns false (early stop) or the ray exits.
+template <class V>
+__device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V& vis) {
+    const int D = tr.depth;
+    const int G = 1 << D;
+    float t = r.tnear;
+    int c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) c[k] = min(max(cell_of(r.o[k], r.dg[k], t), 0), G - 1);
+    uint32_t stk[kMaxDepth + 1];
+    stk[0] = 0u;
+    int L = 0;
+    vis.on_node();
+    while (true) {
+        uint32_t node = stk[L];
+        uint32_t e;
+        int shift;
+        while (true) {
+            shift = D - 1 - L;
+            int oct = (((c[0] >> shift) & 1) << 2) | (((c[1] >> shift) & 1) << 1) | ((c[2] >> shift) & 1);
+            e = __ldg(tr.child + (size_t)node * 8 + oct);
+            if ((e >> 30) != kTagInternal) break;
+            node = e & kIdxMask;
+            ++L;
+            stk[L] = node;
+            vis.on_node();
+        }
+        // the box of entry e: level L+1, 2^shift leaf cells per axis
+        const int size = 1 << shift;
+        int lo[3];
+        float texit = INFINITY;
+        int ax = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = c[k] & ~(size - 1);
+            if (r.dg[k] != 0.f) {
+                float face = (float)(r.dg[k] > 0.f ? lo[k] + size : lo[k]);
+                float te = (face - r.o[k]) * r.inv[k];
+                if (te < texit) {
+                    texit = te;
+                    ax = k;
+                }
+            }
+        }
+        float tout = fminf(texit, r.tfar);
+        if ((e >> 30) == kTagLeaf && tout > t) {
+            if (!vis.on_leaf(e & kIdxMask, t, tout)) return;
+        }
+        if (!(texit < r.tfar)) return;
+        t = texit;
+        int nc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k == ax) {
+                nc[k] = r.dg[k] > 0.f ? lo[k] + size : lo[k] - 1;
+            } else {
+                nc[k] = min(max(cell_of(r.o[k], r.dg[k], t), lo[k]), lo[k] + size - 1);
+            }
+        }
+        if (nc[ax] < 0 || nc[ax] >= G) return;
+        int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
+        L = D - 1 - (31 - __clz(diff));
+        c[0] = nc[0];
+        c[1] = nc[1];
+        c[2] = nc[2];
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// a5: real SH basis, l <= 3, Cartesian form of App. B.1 under the
+// Condon-Shortley reading (Q16); odd-|m| functions are multiplied by odd_sign.
+// ---------------------------------------------------------------------------------
+template <int DEG>
+struct ShDim {
+    static constexpr int B = (DEG + 1) * (DEG + 1);
+};
+
+template <int DEG>
+__device__ __forceinline__ void sh_basis(const float d[3], float odd, float* Y) {
+    const float x = d[0], y = d[1], z = d[2];
+    Y[0] = 0.28209479177387814f;
+    if (DEG >= 1) {
+        Y[1] = odd * 0.48860251190291992f * y;
+        Y[2] = 0.48860251190291992f * z;
+        Y[3] = odd * 0.48860251190291992f * x;
+    }
+    if (DEG >= 2) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        Y[4] = 1.0925484305920792f * x * y;
+        Y[5] = odd * 1.0925484305920792f * y * z;
+        Y[6] = 0.94617469575756008f * zz - 0.31539156525252005f;
+        Y[7] = odd * 1.0925484305920792f * x * z;
+        Y[8] = 0.54627421529603959f * (xx - yy);
+        if (DEG >= 3) {
+            Y[9] = odd * 0.59004358992664352f * y * (3.f * xx - yy);
+            Y[10] = 2.8906114426405538f * x * y * z;
+            Y[11] = odd * 0.45704579946446572f * y * (5.f * zz - 1.f);
+            Y[12] = 0.37317633259011540f * z * (5.f * zz - 3.f);
+            Y[13] = odd * 0.45704579946446572f * x * (5.f * zz - 1.f);
+            Y[14] = 1.4453057213202769f * z * (xx - yy);
+            Y[15] = odd * 0.59004358992664352f * x * (xx - 3.f * yy);
+        }
+    }
+}
+
+// z_ch = sum_b k[b][ch] Y_b over one leaf row (basis-major, channel-minor), fixed order.
+template <int DEG, bool F16>
+__device__ __forceinline__ void sh_dot(const DevTree& tr, uint32_t idx, const float* Y, float z[3]) {
+    constexpr int B = ShDim<DEG>::B;
+    constexpr int NE = 3 * B;
+    z[0] = z[1] = z[2] = 0.f;
+    if (!F16) {
+        const float4* row = reinterpret_cast<const float4*>(static_cast<const float*>(tr.sh) + (size_t)idx * tr.sh_row);
+        constexpr int NV = (NE + 3) / 4;
+        float4 v[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) v[j] = __ldg(row + j);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const float vv[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int el = 4 * j + q;
+                if (el < NE) z[el % 3] = fmaf(vv[q], Y[el / 3], z[el % 3]);
+            }
+        }
+    } else {
+        const uint4* row = reinterpret_cast<const uint4*>(static_cast<const __half*>(tr.sh) + (size_t)idx * tr.sh_row);
+        constexpr int NV = (NE + 7) / 8;
+        uint4 v[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) v[j] = __ldg(row + j);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                __half2 h2 = *reinterpret_cast<const __half2*>(&w4[q]);
+                float2 f = __half22float2(h2);
+                const int el0 = 8 * j + 2 * q, el1 = el0 + 1;
+                if (el0 < NE) z[el0 % 3] = fmaf(f.x, Y[el0 / 3], z[el0 % 3]);
+                if (el1 < NE) z[el1 % 3] = fmaf(f.y, Y[el1 / 3], z[el1 % 3]);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ float sigmoidf_(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
+
+// a4: e = exp(-sigma delta), weight w = T (1 - e), T' = T e.  Explicit _rn intrinsics so
+// every kernel that evaluates a leaf produces bit-identical w, T' (forward, trace,
+// backward passes 1 and 2 must agree on termination and on the prefix sums).
+struct Absorb {
+    float e, w, Tn;
+};
+__device__ __forceinline__ Absorb absorb(float T, float sigma, float delta) {
+    Absorb a;
+    a.e = __expf(-__fmul_rn(sigma, delta));
+    a.w = __fmul_rn(T, __fsub_rn(1.0f, a.e));
+    a.Tn = __fmul_rn(T, a.e);
+    return a;
+}
+
+}  // namespace po

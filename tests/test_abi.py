@@ -1,0 +1,87 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol include/plenoct.h
+declares, and rejects malformed trees / arguments before touching the GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def po():
+    import __graft_entry__ as g
+    g.build()
+    import paper_2103_14024_b200 as po
+    po.lib()
+    return po
+
+
+def test_header_symbols_exported(po):
+    hdr = open(os.path.join(ROOT, "include", "plenoct.h")).read()
+    names = set(re.findall(r"\b(po_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) >= 14
+    L = ctypes.CDLL(po._LIB_PATH)
+    for n in sorted(names):
+        assert hasattr(L, n), n
+    assert set(po.EXPORTS) == names
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2103_14024_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).lower().replace("no cpu", ""), f
+
+
+def _desc(po, depth=2, deg=0, payload=0):
+    return po.TreeDesc((ctypes.c_float * 3)(-1, -1, -1), 2.0, depth, deg, payload, 0, 0)
+
+
+def _create(po, child, sigma, sh, depth=2, deg=0, payload=0):
+    child = np.ascontiguousarray(child, np.uint32)
+    sigma = np.ascontiguousarray(sigma, np.float32)
+    sh = np.ascontiguousarray(sh, np.float32)
+    h = ctypes.c_void_p()
+    d = _desc(po, depth, deg, payload)
+    st = po.lib().po_tree_create(ctypes.byref(d), child.ctypes.data, child.shape[0], sigma.ctypes.data,
+                                 sh.ctypes.data, sigma.shape[0], ctypes.byref(h))
+    return st, po.lib().po_last_error().decode()
+
+
+def test_rejects_malformed_trees(po):
+    L = 2 << 30
+    I = 1 << 30
+    ok_sh = np.zeros((2, 1, 3))
+    # leaf index out of range
+    st, msg = _create(po, [[L | 0, L | 5, 0, 0, 0, 0, 0, 0]], [1, 1], ok_sh, depth=1)
+    assert st == 2 and "out of range" in msg
+    # leaf referenced twice
+    st, msg = _create(po, [[L | 0, L | 0, 0, 0, 0, 0, 0, 0]], [1, 1], ok_sh, depth=1)
+    assert st == 2 and "twice" in msg
+    # internal node deeper than max_depth allows
+    st, msg = _create(po, [[I | 1] + [0] * 7, [L | 0] + [0] * 7], [1], np.zeros((1, 1, 3)), depth=1)
+    assert st == 2 and "max_depth" in msg
+    # unreachable node
+    st, msg = _create(po, [[L | 0] + [0] * 7, [0] * 8], [1], np.zeros((1, 1, 3)), depth=2)
+    assert st == 2 and "unreachable" in msg
+    # NaN payload
+    st, msg = _create(po, [[L | 0] + [0] * 7], [np.nan], np.zeros((1, 1, 3)), depth=1)
+    assert st == 2 and "not finite" in msg
+    st, msg = _create(po, [[L | 0] + [0] * 7], [1.0], np.full((1, 1, 3), np.inf), depth=1)
+    assert st == 2 and "not finite" in msg
+    # unsupported degree / bad depth
+    st, _ = _create(po, [[0] * 8], [], np.zeros((0, 25, 3)), depth=1, deg=4)
+    assert st == 5
+    st, _ = _create(po, [[0] * 8], [], np.zeros((0, 1, 3)), depth=0)
+    assert st == 1
+
+
+def test_rejects_bad_args_without_gpu(po):
+    o = po._opts(2.0, (1, 1, 1))   # gamma outside [0,1]
+    st = po.lib().po_render_rays(None, None, 1, ctypes.byref(o), None, None, None)
+    assert st == 1

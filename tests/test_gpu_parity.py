@@ -1,0 +1,339 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the pinned CPU oracle.
+
+Bars (BASELINE.json north_star; readings Q26-Q29 in DESIGN.md):
+* visited-leaf sequences bit-exact on tie-free rays;
+* RGB max abs error <= 1e-4 (fp32 payload), <= 2e-3 vs fp32 values for the fp16 payload
+  and <= 1e-4 vs the dequantised fp16 values;
+* gradients: per tensor relative L2 <= 1e-3 and per component
+  |d| <= 1e-3 |ref| + 1e-6 max|ref|.
+"""
+import numpy as np
+import pytest
+
+import gen
+from conftest import make_tree, rng
+
+pytestmark = pytest.mark.gpu
+
+RGB_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def env(oracle_mod):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+    import paper_2103_14024_b200 as po
+    return po, oracle_mod, torch
+
+
+def _dev(torch, a, dtype=None):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).cuda()
+
+
+def _tie_free(om, ot, rays, gamma):
+    return om.tie_flags(ot, rays, gamma=gamma if gamma > 0 else 1e-30) == 0
+
+
+def _grad_ok(a, b, tag):
+    a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
+    rel = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+    assert rel <= 1e-3, f"{tag}: rel L2 {rel:.3e}"
+    tol = 1e-3 * np.abs(b) + 1e-6 * np.abs(b).max()
+    bad = np.abs(a - b) > tol
+    assert not bad.any(), f"{tag}: {bad.sum()} components outside tolerance, worst {np.abs(a - b).max():.3e}"
+
+
+# ------------------------------------------------------------------------------------------
+# forward
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("gamma", [0.01, 0.0])
+def test_c0_render_camera(env, c0_tree, gamma):
+    po, om, torch = env
+    tree = po.tree_from_gen(c0_tree)
+    cam, W, H = gen.config_camera("c0")
+    img = po.po_render(tree, po.cams_tensor(cam), W, H, gamma=gamma).reshape(-1, 3).cpu().numpy()
+    ot = om.OracleTree(c0_tree)
+    rays = om.camera_rays(cam, W, H)
+    ref = om.render(ot, rays, gamma=gamma)
+    ok = _tie_free(om, ot, rays, gamma)
+    assert ok.sum() > 4000
+    err = np.abs(img[ok] - ref["rgb"][ok]).max()
+    assert err <= RGB_TOL, err
+    # rays excluded as ties still render sanely
+    assert np.abs(img - ref["rgb"]).max() <= 0.02
+
+
+@pytest.mark.parametrize("gamma", [0.01, 0.0])
+def test_c0_trace_bit_exact(env, c0_tree, gamma):
+    po, om, torch = env
+    tree = po.tree_from_gen(c0_tree)
+    cam, W, H = gen.config_camera("c0")
+    rays = om.camera_rays(cam, W, H).astype(np.float32)
+    ids, counts, nodes = po.po_trace(tree, _dev(torch, rays), max_leaves=96, gamma=gamma)
+    ot = om.OracleTree(c0_tree)
+    r64 = rays.astype(np.float64)
+    ref = om.render(ot, r64, gamma=gamma, max_leaves=96)
+    ok = _tie_free(om, ot, r64, gamma)
+    ids, counts, nodes = ids.cpu().numpy(), counts.cpu().numpy(), nodes.cpu().numpy()
+    assert np.array_equal(counts[ok], ref["n_proc"][ok])
+    assert np.array_equal(ids[ok], ref["leaf_ids"][ok])
+    assert np.array_equal(nodes[ok], ref["nodes_met"][ok])
+
+
+@pytest.mark.parametrize("seed,depth,deg", [(1, 4, 0), (2, 5, 1), (3, 6, 2), (4, 7, 3), (5, 3, 3)])
+def test_random_trees_render_rays(env, seed, depth, deg):
+    po, om, torch = env
+    t = gen.scene_random(seed, depth=depth, sh_degree=deg, sigma_scale=3.0)
+    tree = po.tree_from_gen(t)
+    rays = gen.random_rays(seed, 3000, inside_frac=0.15)
+    out = po.po_render_rays(tree, _dev(torch, rays), gamma=0.01, background=(0.3, 0.6, 0.9)).cpu().numpy()
+    ot = om.OracleTree(t)
+    r64 = rays.astype(np.float64)
+    ref = om.render(ot, r64, gamma=0.01, bg=(0.3, 0.6, 0.9), max_leaves=128)
+    ok = _tie_free(om, ot, r64, 0.01)
+    assert np.abs(out[ok] - ref["rgb"][ok]).max() <= RGB_TOL
+    ids, counts, _ = po.po_trace(tree, _dev(torch, rays), max_leaves=128, gamma=0.01)
+    assert np.array_equal(ids.cpu().numpy()[ok], ref["leaf_ids"][ok])
+    assert np.array_equal(counts.cpu().numpy()[ok], ref["n_proc"][ok])
+
+
+def test_axis_aligned_and_inside_rays(env):
+    po, om, torch = env
+    t = gen.scene_random(9, depth=5, sh_degree=1)
+    tree = po.tree_from_gen(t)
+    g = rng(10)
+    rays = []
+    for k in range(3):
+        for s in (1.0, -1.0):
+            for _ in range(50):
+                o = g.uniform(-0.97, 0.97, 3)
+                o[k] = -3.0 * s if g.random() < 0.5 else o[k]
+                d = np.zeros(3)
+                d[k] = s
+                rays.append(np.concatenate([o, d]))
+    rays = np.array(rays, np.float32)
+    out = po.po_render_rays(tree, _dev(torch, rays), gamma=0.0).cpu().numpy()
+    ot = om.OracleTree(t)
+    ref = om.render(ot, rays.astype(np.float64), gamma=0.0)
+    ok = _tie_free(om, ot, rays.astype(np.float64), 0.0)
+    assert ok.sum() > 200
+    assert np.abs(out[ok] - ref["rgb"][ok]).max() <= RGB_TOL
+
+
+def test_edge_cases(env):
+    po, om, torch = env
+    bg = (0.1, 0.7, 0.3)
+    empty = make_tree([[0] * 8], np.zeros(0), np.zeros((0, 1, 3)), 3, 0)
+    tree = po.tree_from_gen(empty)
+    rays = gen.random_rays(11, 100, inside_frac=0.5)
+    out = po.po_render_rays(tree, _dev(torch, rays), background=bg).cpu().numpy()
+    np.testing.assert_allclose(out, np.tile(bg, (100, 1)), atol=0, rtol=0)
+    t = gen.scene_random(12, depth=4, sh_degree=1)
+    tree = po.tree_from_gen(t)
+    odd = np.array([[3, 3, 3, 1, 0, 0],        # miss
+                    [0, 0, 5, 0, 0, 1],        # pointing away
+                    [0.1, 0.2, 0.3, 0, 0, 0],  # zero direction -> background
+                    [0, 0, 0, 0, 0, 1e-30]],   # tiny direction, normalised
+                   np.float32)
+    out = po.po_render_rays(tree, _dev(torch, odd), background=bg).cpu().numpy()
+    np.testing.assert_allclose(out[:3], np.tile(bg, (3, 1)), atol=0)
+    ref = om.render(om.OracleTree(t), odd[3:].astype(np.float64), bg=bg)
+    assert np.abs(out[3] - ref["rgb"][0]).max() <= RGB_TOL
+    # n = 0 and an empty camera batch are no-ops
+    po.po_render_rays(tree, torch.zeros((0, 6), device="cuda"))
+    # ragged image size (not a multiple of the 16x16 CTA tile)
+    cam = gen.orbit_camera(3.0, 10.0, 20.0, 37, 23, 40.0)
+    img = po.po_render(tree, po.cams_tensor(cam), 37, 23).reshape(-1, 3).cpu().numpy()
+    rr = om.camera_rays(cam, 37, 23)
+    ref = om.render(om.OracleTree(t), rr)
+    ok = _tie_free(om, om.OracleTree(t), rr, 0.01)
+    assert np.abs(img[ok] - ref["rgb"][ok]).max() <= RGB_TOL
+
+
+def test_multi_view_batch_and_host_path(env, c0_tree):
+    po, om, torch = env
+    tree = po.tree_from_gen(c0_tree)
+    cams = np.concatenate([gen.orbit_camera(3.0, 23.4 + 40 * i, 17.9, 64, 64, 70.0) for i in range(5)])
+    dev = po.po_render(tree, po.cams_tensor(cams), 64, 64).cpu().numpy()
+    host = po.po_render_host(tree, cams, 64, 64)
+    assert np.array_equal(dev, host)
+    ot = om.OracleTree(c0_tree)
+    for i in range(5):
+        rays = om.camera_rays(cams[i:i + 1], 64, 64)
+        ref = om.render(ot, rays)
+        ok = _tie_free(om, ot, rays, 0.01)
+        assert np.abs(dev[i].reshape(-1, 3)[ok] - ref["rgb"][ok]).max() <= RGB_TOL
+
+
+def test_sh_sign_convention(env):
+    po, om, torch = env
+    t = gen.scene_random(13, depth=3, sh_degree=3)
+    rays = gen.random_rays(14, 500)
+    r64 = rays.astype(np.float64)
+    for sign, cs in ((po.PO_SH_CS, 1), (po.PO_SH_NO_CS, 0)):
+        tree = po.tree_from_gen(t, sh_sign=sign)
+        out = po.po_render_rays(tree, _dev(torch, rays)).cpu().numpy()
+        ot = om.OracleTree(t, sh_cs=cs)
+        ref = om.render(ot, r64)
+        ok = _tie_free(om, ot, r64, 0.01)
+        assert np.abs(out[ok] - ref["rgb"][ok]).max() <= RGB_TOL
+
+
+def test_fp16_payload(env):
+    po, om, torch = env
+    t = gen.scene_random(15, depth=6, sh_degree=3, sigma_scale=3.0)
+    tree = po.tree_from_gen(t, payload=po.PO_F16)
+    rays = gen.random_rays(16, 4000)
+    r64 = rays.astype(np.float64)
+    out = po.po_render_rays(tree, _dev(torch, rays)).cpu().numpy()
+    deq = t.sh.astype(np.float16).astype(np.float64)       # round-to-nearest-even (reading Q20)
+    ot_q = om.OracleTree(t, sh=deq)
+    ref_q = om.render(ot_q, r64)
+    ok = _tie_free(om, ot_q, r64, 0.01)
+    assert np.abs(out[ok] - ref_q["rgb"][ok]).max() <= RGB_TOL            # kernel correctness (Q29 check 1)
+    ref = om.render(om.OracleTree(t), r64)
+    ok2 = ok & _tie_free(om, om.OracleTree(t), r64, 0.01)
+    assert np.abs(out[ok2] - ref["rgb"][ok2]).max() <= 2e-3              # quantisation budget (Q29 check 2)
+    s, k = tree.read_leaves()
+    np.testing.assert_array_equal(k, deq.astype(np.float32))
+
+
+def test_c1_sampled_pixels_full_launch(env, c1_tree):
+    """c1 at full size in the bench's launch configuration; oracle on 4096 sampled pixels."""
+    po, om, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    cam, W, H = gen.config_camera("c1")
+    img = po.po_render(tree, po.cams_tensor(cam), W, H, gamma=0.01).reshape(-1, 3).cpu().numpy()
+    rays = om.camera_rays(cam, W, H)
+    pick = rng(17).choice(W * H, 4096, replace=False)
+    ot = om.OracleTree(c1_tree)
+    ref = om.render(ot, rays[pick], gamma=0.01)
+    ok = _tie_free(om, ot, rays[pick], 0.01)
+    # at depth 9 ~27% of rays have two plane crossings within 1e-6*edge (reading Q27 (i))
+    assert ok.sum() > 2500
+    assert np.abs(img[pick][ok] - ref["rgb"][ok]).max() <= RGB_TOL
+    print(f"c1 sample: {ok.sum()} tie-free of 4096, all-ray max err {np.abs(img[pick] - ref['rgb']).max():.3e}")
+    # whole-frame property: every pixel is a convex combination of colours in (0,1) and white
+    assert np.all(img >= 0) and np.all(img <= 1.0 + 1e-6)
+    # counters of the same traversal match the oracle's per-ray counts on the sample
+    st = po.po_render_stats(tree, po.cams_tensor(cam), W, H)
+    assert st["hit_rays"] > 0.3 * W * H
+
+
+def test_stats_match_oracle_c0(env, c0_tree):
+    po, om, torch = env
+    tree = po.tree_from_gen(c0_tree)
+    cam, W, H = gen.config_camera("c0")
+    st = po.po_render_stats(tree, po.cams_tensor(cam), W, H)
+    ot = om.OracleTree(c0_tree)
+    rays = om.camera_rays(cam, W, H)
+    ref = om.render(ot, rays)
+    assert np.all(_tie_free(om, ot, rays, 0.01))
+    assert st["leaf_visits"] == int(ref["n_proc"].sum())
+    assert st["nodes"] == int(ref["nodes_met"].sum())
+    assert st["hit_rays"] == int((ref["nodes_met"] > 0).sum())
+
+
+# ------------------------------------------------------------------------------------------
+# backward
+# ------------------------------------------------------------------------------------------
+def _backward_case(env, t, rays, gamma, use_aux, seed):
+    po, om, torch = env
+    tree = po.tree_from_gen(t)
+    r = _dev(torch, rays)
+    g = rng(seed).normal(size=(rays.shape[0], 3)).astype(np.float32)
+    gs = torch.zeros(tree.n_leaves, device="cuda")
+    gk = torch.zeros((tree.n_leaves, tree.B, 3), device="cuda")
+    aux = None
+    if use_aux:
+        aux = torch.empty((rays.shape[0], 4), dtype=torch.float64, device="cuda")
+        po.po_render_rays(tree, r, aux=aux, gamma=gamma)
+    po.po_render_backward(tree, r, _dev(torch, g), gs, gk, aux=aux, gamma=gamma)
+    rs, rk = om.backward(om.OracleTree(t), rays.astype(np.float64), g.astype(np.float64), gamma=gamma)
+    _grad_ok(gs.cpu().numpy(), rs, "sigma")
+    _grad_ok(gk.cpu().numpy(), rk, "sh")
+
+
+@pytest.mark.parametrize("gamma,use_aux", [(0.0, False), (0.0, True), (0.01, False), (0.01, True)])
+def test_c0_backward(env, c0_tree, gamma, use_aux):
+    po, om, torch = env
+    cam, W, H = gen.config_camera("c0")
+    rays = om.camera_rays(cam, W, H)
+    ot = om.OracleTree(c0_tree)
+    ok = _tie_free(om, ot, rays, gamma)
+    _backward_case(env, c0_tree, rays[ok].astype(np.float32), gamma, use_aux, 21)
+
+
+@pytest.mark.parametrize("seed,deg", [(31, 1), (32, 2), (33, 3), (34, 0)])
+def test_random_tree_backward(env, seed, deg):
+    po, om, torch = env
+    t = gen.scene_random(seed, depth=5, sh_degree=deg)
+    rays = gen.random_rays(seed, 2000, inside_frac=0.1)
+    ot = om.OracleTree(t)
+    ok = _tie_free(om, ot, rays.astype(np.float64), 1e-30)
+    _backward_case(env, t, rays[ok], 0.0, False, seed)
+
+
+def test_backward_fd_c0(env, c0_tree):
+    """GPU gradient vs central finite differences of the oracle's forward (north_star check)."""
+    po, om, torch = env
+    cam, W, H = gen.config_camera("c0")
+    rays = om.camera_rays(cam, W, H)
+    ot = om.OracleTree(c0_tree)
+    ok = np.flatnonzero(_tie_free(om, ot, rays, 1e-30) & (om.render(ot, rays)["n_proc"] > 0))
+    sub = rays[rng(40).choice(ok, 64, replace=False)].astype(np.float32)
+    tree = po.tree_from_gen(c0_tree)
+    g = rng(41).normal(size=(64, 3))
+    gs = torch.zeros(tree.n_leaves, device="cuda")
+    gk = torch.zeros((tree.n_leaves, 4, 3), device="cuda")
+    po.po_render_backward(tree, _dev(torch, sub), _dev(torch, g, np.float32), gs, gk, gamma=0.0)
+    gs, gk = gs.cpu().numpy(), gk.cpu().numpy()
+    r64 = sub.astype(np.float64)
+    fw = om.render(ot, r64, gamma=0.0, max_leaves=128)
+    touched = np.unique(fw["leaf_ids"][fw["leaf_ids"] >= 0])
+    pick = rng(42).choice(touched, 24, replace=False)
+    sig0, sh0 = c0_tree.sigma.astype(np.float64), c0_tree.sh.astype(np.float64)
+    g32 = g.astype(np.float32).astype(np.float64)
+
+    def L(s, k):
+        return float((om.render(om.OracleTree(c0_tree, sigma=s, sh=k), r64, gamma=0.0)["rgb"] * g32).sum())
+    a, f = [], []
+    for lf in pick:
+        if sig0[lf] > 1e-3:
+            h = 1e-6 * max(1, abs(sig0[lf]))
+            sp, sm = sig0.copy(), sig0.copy()
+            sp[lf] += h
+            sm[lf] -= h
+            a.append(gs[lf]); f.append((L(sp, sh0) - L(sm, sh0)) / (2 * h))
+        for b in range(4):
+            h = 1e-6 * max(1, abs(sh0[lf, b, 0]))
+            kp, km = sh0.copy(), sh0.copy()
+            kp[lf, b, 0] += h
+            km[lf, b, 0] -= h
+            a.append(gk[lf, b, 0]); f.append((L(sig0, kp) - L(sig0, km)) / (2 * h))
+    _grad_ok(a, f, "fd")
+
+
+def test_loss_grad_and_sgd(env):
+    po, om, torch = env
+    t = gen.scene_random(50, depth=4, sh_degree=1)
+    tree = po.tree_from_gen(t)
+    pred = torch.rand((1000, 3), device="cuda")
+    tgt = torch.rand((1000, 3), device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g = po.po_l2_loss_grad(pred, tgt, loss=loss)
+    diff = (pred - tgt).double().cpu().numpy()
+    np.testing.assert_allclose(g.cpu().numpy(), 2 * diff, rtol=1e-6, atol=1e-7)
+    assert abs(loss.item() - (diff ** 2).sum()) < 1e-9 * max(1, (diff ** 2).sum())
+    gs = torch.randn(tree.n_leaves, device="cuda")
+    gk = torch.randn((tree.n_leaves, tree.B, 3), device="cuda")
+    po.po_tree_sgd_step(tree, gs, gk, 0.25)
+    s, k = tree.read_leaves()
+    np.testing.assert_allclose(s, t.sigma - 0.25 * gs.cpu().numpy(), rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(k, t.sh - 0.25 * gk.cpu().numpy(), rtol=1e-6, atol=1e-6)
+    tq = po.tree_from_gen(t, payload=po.PO_F16)
+    with pytest.raises(po.PoError):
+        po.po_tree_sgd_step(tq, gs, gk, 0.25)
