@@ -245,6 +245,101 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_c4(args):
+    """Config c4: direct-optimisation step (forward + Eq. 3 gradient + backward + SUM allreduce +
+    SGD), 1,048,576 rays per GPU per step (8 M at 8 GPUs), gamma = 0 (reading Q12)."""
+    import numpy as np
+    import torch
+    import gen
+    import paper_2103_14024_b200 as po
+    from paper_2103_14024_b200.optim import OctreeOptimizer
+
+    ws, rank, local = _dist()
+    group = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t_gt = gen.scene_c1()
+    gt = po.tree_from_gen(t_gt, device=local)
+    g = np.random.Generator(np.random.Philox(key=1))
+    sig = (t_gt.sigma + g.normal(0.0, 0.1 * 768.0, t_gt.sigma.shape)).astype(np.float32)
+    sh = (t_gt.sh + g.normal(0.0, 0.1, t_gt.sh.shape)).astype(np.float32)
+    tree = po.po_tree_create(t_gt.child, sig, sh, t_gt.depth, 3, t_gt.bbox_min, t_gt.edge, device=local)
+    cams = gen.fibonacci_hemisphere(100, 4.0, W, H, 1111.111)
+    n_rays = args.rays
+    batches = []
+    for s in range(args.warmup + args.steps):
+        rg = np.random.Generator(np.random.Philox(key=2 + s * ws + rank))
+        pick = rg.choice(100 * W * H, size=n_rays, replace=False)
+        rays = torch.from_numpy(gen.camera_rays_f32(cams, W, H, pick // (W * H), pick % (W * H))).to(dev)
+        tgt = po.po_render_rays(gt, rays, gamma=0.0)   # targets: renders of the unperturbed tree
+        batches.append((rays, tgt))
+    torch.cuda.synchronize()
+    gt.destroy()
+    opt = OctreeOptimizer(tree, lr=args.lr, gamma=0.0, device=dev)
+    # algorithmic bytes of the dominant kernel (k_backward, pass 2 with aux) over the timed batches
+    visits = nodes = 0
+    for rays, _ in batches[args.warmup:]:
+        _, cnt, nd = po.po_trace(tree, rays, max_leaves=0, gamma=0.0)
+        visits += int(cnt.sum().item())
+        nodes += int(nd.sum().item())
+    for s in range(args.warmup):
+        opt.step(*batches[s])
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    l0 = po.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    losses = []
+    for s in range(args.warmup, args.warmup + args.steps):
+        losses.append(opt.step(*batches[s]).clone())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    launches = po.launch_count() - l0
+    clk = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    t_max = t_ms
+    if ws > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    K = args.steps
+    rays_per_s = ws * K * n_rays / (t_max / 1e3)
+    if rank == 0:
+        peak, peak_src = _peaks()
+        alg = (visits * (4 + 192 + 196) + nodes * 32) / K + n_rays * (24 + 12 + 32)
+        line = {
+            "metric": "direct octree optimisation rays/s (c4: forward+backward+allreduce+SGD)",
+            "value": round(rays_per_s, 1), "unit": "rays/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
+            "ms_per_step": round(t_max / K, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (c1 tree perturbed; targets = renders of the unperturbed tree)",
+            "config": {"workload": f"c4: {n_rays} rays per GPU per step from 100 Fibonacci-hemisphere 800x800 views, "
+                                   "gamma 0, SGD lr %g" % args.lr, "parallelism": f"ray data-parallel x{ws}, "
+                                   "tree replicated, bucketed NCCL SUM allreduce"},
+            "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
+            "leaf_visits_per_step": visits / K,
+            "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+                         "alg_bytes_per_step": round(alg),
+                         "achieved_step": round(alg / (t_max / K / 1e3) / 1e9, 1),
+                         "alg_bytes_def": "visits*(4 sigma + 192 SH row + 196 gradient RMW) + nodes*32 + rays*68"},
+            "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
 def cpu_baseline(t_gen, seconds: float = 15.0, max_frames: int = 200):
     """The oracle as it stands, on this host's cores, on whole c1 frames (bounded by ~seconds)."""
     import numpy as np
@@ -311,11 +406,16 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["c1", "c4"], default="c1")
+    ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
+    ap.add_argument("--lr", type=float, default=1e-4, help="c4: SGD learning rate (loss is a sum over rays)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c4":
+        run_c4(args)
     else:
         run_ours(args)
 

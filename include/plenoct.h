@@ -106,6 +106,13 @@ po_status po_render(const po_tree* tree, const po_camera* cams, int32_t n_cams, 
 po_status po_render_host(const po_tree* tree, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
                          const po_render_opts* opts, float* out_rgb_host, po_stream stream);
 
+/* a1 on its own: the exact fp32 rays po_render generates, device float[n_cams][H][W][6] =
+ * (origin, un-normalised direction R d_cam).  po_render(cams) equals po_render_rays(these rays)
+ * bit for bit.  Each component is an IEEE round-to-nearest evaluation of
+ * dx = ((i + 0.5) - cx) / fx, dy = -(((j + 0.5) - cy) / fy), d_k = (R_k0 dx + R_k1 dy) - R_k2. */
+po_status po_camera_rays(const po_camera* cams, int32_t n_cams, int32_t W, int32_t H, float* rays, int32_t device,
+                         po_stream stream);
+
 /* Forward render of explicit rays.
  * rays     device float[n][6] = (origin xyz, direction xyz); the direction is normalised
  *          by the library (zero direction => that ray returns the background).
@@ -138,6 +145,12 @@ po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, flo
  * sigma~ -= lr * grad_sigma, k -= lr * grad_sh.  PO_ERR_UNSUPPORTED for fp16 payloads. */
 po_status po_tree_sgd_step(po_tree* tree, const float* grad_sigma, const float* grad_sh, float lr,
                            po_stream stream);
+/* Same update restricted to parameter indices [begin, end) of the index space
+ * [0, n_leaves) = sigma~ of leaf i, n_leaves + j = j-th element of grad_sh / sh (leaf-major,
+ * [B][3] within a leaf).  Lets the caller update each gradient bucket as soon as its
+ * allreduce has landed (a9 overlap).  PO_ERR_INVALID_ARG if the range is outside. */
+po_status po_tree_sgd_step_range(po_tree* tree, const float* grad_sigma, const float* grad_sh, float lr,
+                                 int64_t begin, int64_t end, po_stream stream);
 
 /* ---- parity / measurement helpers ----------------------------------------------------
  * po_trace: the visited-leaf sequence of each ray up to termination (same traversal as

@@ -138,8 +138,13 @@ def backward(ot: OracleTree, rays, dL_dC, gamma: float = 0.0, bg=(1.0, 1.0, 1.0)
     return gs, gk
 
 
-def tie_flags(ot: OracleTree, rays, gamma: float = 0.01, tol_plane: float = 1e-6, tol_gamma: float = 1e-4,
+def tie_flags(ot: OracleTree, rays, gamma: float = 0.01, tol_plane: float = 1e-6, tol_gamma: float = 2e-2,
               nthreads: int = 0) -> np.ndarray:
+    """Tie tags of DESIGN.md reading Q27.  tol_gamma = 2e-2 (not the survey's 1e-4): an fp32 ray
+    (origin, direction rounded to fp32, crossings at t ~ 3-4) carries segment-length errors
+    e_delta ~ 1e-6 world units, so with sigma up to 768 (c1, sigma_max h = 3) and up to ~15
+    segments before termination T is only known to ~ sigma_max * N * e_delta ~ 1e-2 relative;
+    rays whose T passes within that band of gamma can legitimately stop one segment apart."""
     rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
     f = np.zeros(rays.shape[0], np.uint8)
     lib().or_tie_flags(ot.ref, _ptr(rays), rays.shape[0], gamma, tol_plane, tol_gamma, _ptr(f), nthreads)

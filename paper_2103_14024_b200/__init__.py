@@ -24,8 +24,9 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
           5: "PO_ERR_UNSUPPORTED"}
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_destroy", "po_tree_info",
-           "po_tree_read_leaves", "po_render", "po_render_host", "po_render_rays", "po_render_backward",
-           "po_l2_loss_grad", "po_tree_sgd_step", "po_trace", "po_render_stats"]
+           "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
+           "po_render_backward",
+           "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats"]
 
 
 class PoError(RuntimeError):
@@ -65,9 +66,11 @@ def lib():
         L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_host.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_rays.argtypes = [P, P, I64, P, P, P, P]
+        L.po_camera_rays.argtypes = [P, I32, I32, I32, P, I32, P]
         L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P]
         L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
         L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
+        L.po_tree_sgd_step_range.argtypes = [P, P, P, F, I64, I64, P]
         L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, P]
         L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
         for name in EXPORTS:
@@ -207,6 +210,16 @@ def po_render_host(tree: PlenOctree, cams_host: np.ndarray, W: int, H: int, out_
     return out_host
 
 
+def po_camera_rays(cams, W: int, H: int, stream=None):
+    """The exact fp32 rays po_render generates: CUDA float32 [n][H][W][6] (origin, un-normalised d)."""
+    import torch
+    cams = _need(cams, torch.float32, (16,))
+    rays = torch.empty((cams.shape[0], H, W, 6), dtype=torch.float32, device=cams.device)
+    _check(lib().po_camera_rays(_ptr(cams), cams.shape[0], W, H, _ptr(rays), cams.device.index or 0,
+                                _stream(stream)))
+    return rays
+
+
 def po_render_rays(tree: PlenOctree, rays, out=None, aux=None, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
                    stream=None):
     import torch
@@ -252,6 +265,11 @@ def po_l2_loss_grad(pred, target, dL_dC=None, loss=None, stream=None):
 
 def po_tree_sgd_step(tree: PlenOctree, grad_sigma, grad_sh, lr: float, stream=None):
     _check(lib().po_tree_sgd_step(tree.handle, _ptr(grad_sigma), _ptr(grad_sh), float(lr), _stream(stream)))
+
+
+def po_tree_sgd_step_range(tree: PlenOctree, grad_sigma, grad_sh, lr: float, begin: int, end: int, stream=None):
+    _check(lib().po_tree_sgd_step_range(tree.handle, _ptr(grad_sigma), _ptr(grad_sh), float(lr), int(begin), int(end),
+                                        _stream(stream)))
 
 
 def po_trace(tree: PlenOctree, rays, max_leaves: int = 64, gamma: float = 0.01, with_nodes: bool = True,

@@ -25,6 +25,14 @@ struct po_tree {
     void* d_sh = nullptr;
     po_camera* d_cams = nullptr;   // scratch for po_render_host
     int cam_cap = 0;
+    float* d_img = nullptr;        // scratch image for po_render_host
+    size_t img_cap = 0;
+    // work counters of the persistent render kernel: kWorkSlots pairs, handed out round
+    // robin so up to kWorkSlots renders of one tree may be in flight on different streams
+    static constexpr int kWorkSlots = 64;
+    unsigned* d_work = nullptr;
+    std::atomic<uint32_t> work_rr{0};
+    unsigned* next_work() { return d_work + 2 * (work_rr.fetch_add(1) % kWorkSlots); }
 };
 
 namespace {
@@ -123,8 +131,8 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     if (desc->sh_sign != PO_SH_CS && desc->sh_sign != PO_SH_NO_CS)
         return fail(PO_ERR_INVALID_ARG, "sh_sign %d invalid", desc->sh_sign);
     if (n_nodes < 1 || !child) return fail(PO_ERR_INVALID_ARG, "need n_nodes >= 1 and a child table");
-    if (n_leaves < 0 || n_leaves > (int64_t)po::kIdxMask + 1 || n_nodes > (int64_t)po::kIdxMask + 1)
-        return fail(PO_ERR_INVALID_ARG, "n_leaves / n_nodes out of range");
+    if (n_leaves < 0 || n_leaves > (int64_t)po::kIdxMask + 1 || n_nodes > ((int64_t)1 << 29))
+        return fail(PO_ERR_INVALID_ARG, "n_leaves (<= 2^30) / n_nodes (<= 2^29) out of range");
     if (n_leaves > 0 && (!sigma || !sh)) return fail(PO_ERR_INVALID_ARG, "sigma / sh NULL with n_leaves > 0");
 
     // ---- structural validation: BFS from the root with levels ----
@@ -198,6 +206,10 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sigma)"));
     e = cudaMalloc(&t->d_sh, (size_t)std::max<int64_t>(n_leaves, 1) * row * elt);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
+    e = cudaMalloc(&t->d_work, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
+    e = cudaMemset(t->d_work, 0, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "memset(work)"));
     e = cudaMemcpy(t->d_child, child, (size_t)n_nodes * 8 * sizeof(uint32_t), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "upload child"));
     if (n_leaves > 0) {
@@ -235,6 +247,8 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_sigma) cudaFree(t->d_sigma);
     if (t->d_sh) cudaFree(t->d_sh);
     if (t->d_cams) cudaFree(t->d_cams);
+    if (t->d_work) cudaFree(t->d_work);
+    if (t->d_img) cudaFree(t->d_img);
     t->d_child = nullptr;
     delete t;
     return PO_OK;
@@ -304,7 +318,7 @@ po_status po_render(const po_tree* t, const po_camera* cams, int32_t n_cams, int
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
-                                      out_rgb, (cudaStream_t)stream),
+                                      out_rgb, const_cast<po_tree*>(t)->next_work(), (cudaStream_t)stream),
                     "po_render");
 }
 
@@ -331,21 +345,37 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
     }
     cudaError_t e = cudaMemcpyAsync(t->d_cams, cams_host, sizeof(po_camera) * (size_t)n_cams, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_status(e, "H2D cams");
-    float* d_out = nullptr;
     const size_t out_bytes = (size_t)n_cams * W * H * 3 * sizeof(float);
-    e = cudaMallocAsync((void**)&d_out, out_bytes, s);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(out)");
+    if (t->img_cap < out_bytes) {   // grows once; later calls reuse it (no per-call allocation)
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_status(e, "sync");
+        if (t->d_img) cudaFree(t->d_img);
+        t->d_img = nullptr;
+        t->img_cap = 0;
+        e = cudaMalloc((void**)&t->d_img, out_bytes);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(image)");
+        t->img_cap = out_bytes;
+    }
     po_status st = launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, t->d_cams,
-                                              n_cams, W, H, o, d_out, s),
+                                              n_cams, W, H, o, t->d_img, t->next_work(), s),
                             "po_render_host");
     if (st == PO_OK) {
-        e = cudaMemcpyAsync(out_host, d_out, out_bytes, cudaMemcpyDeviceToHost, s);
+        e = cudaMemcpyAsync(out_host, t->d_img, out_bytes, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) st = cuda_status(e, "D2H image");
     }
-    cudaFreeAsync(d_out, s);
     e = cudaStreamSynchronize(s);
     if (st == PO_OK && e != cudaSuccess) st = cuda_status(e, "sync");
     return st;
+}
+
+po_status po_camera_rays(const po_camera* cams, int32_t n_cams, int32_t W, int32_t H, float* rays, int32_t device,
+                         po_stream stream) {
+    if (po_status s = check_image(n_cams, W, H)) return s;
+    if (n_cams == 0) return PO_OK;
+    if (!cams || !rays) return fail(PO_ERR_INVALID_ARG, "cams / rays NULL");
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_camera_rays(cams, n_cams, W, H, rays, (cudaStream_t)stream), "po_camera_rays");
 }
 
 po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, float* out_rgb,
@@ -388,17 +418,27 @@ po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, flo
     return launched(po::launch_l2_loss(pred, target, n * 3, dL_dC, loss, (cudaStream_t)stream), "po_l2_loss_grad");
 }
 
-po_status po_tree_sgd_step(po_tree* t, const float* grad_sigma, const float* grad_sh, float lr, po_stream stream) {
+po_status po_tree_sgd_step_range(po_tree* t, const float* grad_sigma, const float* grad_sh, float lr, int64_t begin,
+                                 int64_t end, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
     if (t->desc.payload != PO_F32) return fail(PO_ERR_UNSUPPORTED, "SGD needs an fp32 payload (P:973 trains in fp32)");
     if (!std::isfinite(lr)) return fail(PO_ERR_INVALID_ARG, "lr not finite");
-    if (t->n_leaves == 0) return PO_OK;
+    const int64_t total = t->n_leaves * (int64_t)(t->ne + 1);
+    if (begin < 0 || end > total || begin > end)
+        return fail(PO_ERR_INVALID_ARG, "range [%lld, %lld) outside [0, %lld)", (long long)begin, (long long)end,
+                    (long long)total);
+    if (end == begin) return PO_OK;
     if (!grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL gradient");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_sgd(t->d_sigma, static_cast<float*>(t->d_sh), t->sh_row, t->ne, t->n_leaves, grad_sigma,
-                                   grad_sh, lr, (cudaStream_t)stream),
+                                   grad_sh, lr, begin, end, (cudaStream_t)stream),
                     "po_tree_sgd_step");
+}
+
+po_status po_tree_sgd_step(po_tree* t, const float* grad_sigma, const float* grad_sh, float lr, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    return po_tree_sgd_step_range(t, grad_sigma, grad_sh, lr, 0, t->n_leaves * (int64_t)(t->ne + 1), stream);
 }
 
 po_status po_trace(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, int32_t max_leaves,

@@ -9,6 +9,8 @@
 //   k_l2_loss, k_sgd         Eq. (3) gradient helper and the SGD update
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "traverse.cuh"
 
@@ -30,10 +32,10 @@ struct FwdVisitor {
     __device__ __forceinline__ void on_node() {}
     __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
         const float st = __ldg(tr.sigma + idx);
-        if (!(st > 0.f)) return true;   // sigma = (sigma~)_+ = 0: alpha = 0 (reading Q10)
-        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
         float z[3];
-        sh_dot<DEG, F16>(tr, idx, Y, z);
+        sh_dot<DEG, F16>(tr, idx, Y, z);   // row loads issued together with the sigma load
+        if (!(st > 0.f)) return true;      // sigma = (sigma~)_+ = 0: alpha = 0 (reading Q10)
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(a.w, sigmoidf_(z[ch]), C[ch]);
         T = a.Tn;
@@ -165,13 +167,38 @@ __device__ __forceinline__ void camera_ray(const po_camera* __restrict__ cams, i
     float c[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) c[k] = __ldg(cm + k);
-    const float dx = ((float)px + 0.5f - c[14]) / c[12];
-    const float dy = -((float)py + 0.5f - c[15]) / c[13];
+    // explicit round-to-nearest ops (no FMA contraction): the ray is reproducible bit for bit
+    // by any IEEE fp32 implementation of the same expression (po_camera_rays exports it)
+    const float dx = __fdiv_rn(__fsub_rn(__fadd_rn((float)px, 0.5f), c[14]), c[12]);
+    const float dy = -__fdiv_rn(__fsub_rn(__fadd_rn((float)py, 0.5f), c[15]), c[13]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        d[k] = c[k * 4 + 0] * dx + c[k * 4 + 1] * dy - c[k * 4 + 2];
+        d[k] = __fsub_rn(__fadd_rn(__fmul_rn(c[k * 4 + 0], dx), __fmul_rn(c[k * 4 + 1], dy)), c[k * 4 + 2]);
         o[k] = c[k * 4 + 3];
     }
+}
+
+__global__ void __launch_bounds__(256) k_camera_rays(const po_camera* __restrict__ cams, int n_cams, int W, int H,
+                                                     float* __restrict__ rays) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per = (int64_t)W * H;
+    if (i >= per * n_cams) return;
+    const int view = (int)(i / per);
+    const int p = (int)(i - (int64_t)view * per);
+    float o[3], d[3];
+    camera_ray(cams, view, p % W, p / W, o, d);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        rays[i * 6 + k] = o[k];
+        rays[i * 6 + 3 + k] = d[k];
+    }
+}
+
+cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, float* rays, cudaStream_t s) {
+    const int64_t n = (int64_t)W * H * n_cams;
+    if (n == 0) return cudaSuccess;
+    k_camera_rays<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cams, n_cams, W, H, rays);
+    return cudaGetLastError();
 }
 
 // CTA = 16x16 pixels = 8 warps, each warp an 8x4 pixel tile (warp-coherent ray packets).
@@ -182,31 +209,87 @@ __device__ __forceinline__ bool tile_pixel(int W, int H, int& px, int& py) {
     return px < W && py < H;
 }
 
-template <int DEG, bool F16>
-__global__ void __launch_bounds__(256) k_render(DevTree tr, const po_camera* __restrict__ cams, int W, int H,
-                                                RenderOpts opt, float* __restrict__ out) {
-    int px, py;
-    if (!tile_pixel(W, H, px, py)) return;
-    const int view = blockIdx.z;
-    float o[3], d[3];
-    camera_ray(cams, view, px, py, o, d);
-    RayState r;
-    float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
-    if (ray_setup(tr, o, d, r)) {
-        FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-        traverse(tr, r, v);
+// Persistent render: grid = #SMs x resident CTAs.  Work = 16x16-pixel blocks (8 warp tiles
+// of 8x4 pixels, raster order over views x block rows x block columns), claimed from a
+// global counter one block per CTA "slot".  Inside a CTA the warps take warp tiles from a
+// shared ticket counter: ticket k -> slot k/8, tile k%8; the warp drawing tile 0 of a slot
+// claims that slot's block and publishes it.  So a CTA's warps stay on one or two
+// neighbouring blocks (rays of a CTA share nodes and leaves in L1) while no warp ever waits
+// for a slower one, and the uneven per-block cost (misses vs. surface hits) is balanced
+// across SMs with no tail wave.  The last CTA to finish resets the global counters
+// (work[0] = next block, work[1] = finished CTAs) for the next launch on the stream.
+constexpr int kSlotRing = 16;
+template <int DEG, bool F16, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camera* __restrict__ cams, int n_cams, int W,
+                                                int H, RenderOpts opt, float* __restrict__ out,
+                                                unsigned* __restrict__ work) {
+    PO_DECLARE_STACK(stk);
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_block[kSlotRing];
+    __shared__ volatile unsigned s_pub[kSlotRing];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_ticket = 0;
+    if (threadIdx.x < kSlotRing) s_pub[threadIdx.x] = 0xFFFFFFFFu;
+    __syncthreads();
+    const unsigned bx_n = (unsigned)(W + 15) >> 4, by_n = (unsigned)(H + 15) >> 4;
+    const unsigned per_view = bx_n * by_n;
+    const unsigned total = per_view * (unsigned)n_cams;
+    while (true) {
+        unsigned blk = 0, sub = 0;
+        if (lane == 0) {
+            const unsigned k = atomicAdd(&s_ticket, 1u);
+            const unsigned slot = k >> 3;
+            sub = k & 7u;
+            if (sub == 0) {
+                s_block[slot % kSlotRing] = atomicAdd(work, 1u);
+                __threadfence_block();
+                s_pub[slot % kSlotRing] = slot;
+            } else {
+                while (s_pub[slot % kSlotRing] != slot) {
+                }
+                __threadfence_block();
+            }
+            blk = s_block[slot % kSlotRing];
+        }
+        blk = __shfl_sync(0xffffffffu, blk, 0);
+        sub = __shfl_sync(0xffffffffu, sub, 0);
+        if (blk >= total) break;
+        const unsigned view = blk / per_view;
+        const unsigned rem = blk - view * per_view;
+        const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
+        const int px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
+        const int py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
+        if (px < W && py < H) {
+            float o[3], d[3];
+            camera_ray(cams, (int)view, px, py, o, d);
+            RayState r;
+            float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
+            if (ray_setup(tr, o, d, r)) {
+                FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
+                traverse(tr, r, v, stk);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+                for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+            }
+            float* p = out + (((size_t)view * H + py) * W + px) * 3;
+            p[0] = C[0];
+            p[1] = C[1];
+            p[2] = C[2];
+        }
     }
-    float* p = out + (((size_t)view * H + py) * W + px) * 3;
-    p[0] = C[0];
-    p[1] = C[1];
-    p[2] = C[2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            atomicExch(work, 0u);
+            atomicExch(work + 1, 0u);
+        }
+    }
 }
 
 template <int DEG, bool F16>
 __global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                      RenderOpts opt, float* __restrict__ out, double* __restrict__ aux) {
+    PO_DECLARE_STACK(stk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float o[3], d[3];
@@ -221,7 +304,7 @@ __global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __
         float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
         if (hit) {
             FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-            traverse(tr, r, v);
+            traverse(tr, r, v, stk);
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
         }
@@ -232,7 +315,7 @@ __global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __
         float T = 1.f;
         if (hit) {
             TotalVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-            traverse(tr, r, v);
+            traverse(tr, r, v, stk);
             T = v.T;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) C[ch] = v.C[ch] + (double)v.T * (double)opt.bg[ch];
@@ -251,6 +334,7 @@ __global__ void __launch_bounds__(256) k_backward(DevTree tr, const float* __res
                                                   const float* __restrict__ dL_dC, const double* __restrict__ aux,
                                                   RenderOpts opt, float* __restrict__ grad_sigma,
                                                   float* __restrict__ grad_sh) {
+    PO_DECLARE_STACK(stk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float o[3], d[3];
@@ -270,16 +354,17 @@ __global__ void __launch_bounds__(256) k_backward(DevTree tr, const float* __res
         for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = aux[i * 4 + ch];
     } else {   // pass 1: total = sum_{k<=N} c_k w_k including the background
         TotalVisitor<DEG, F16> tv(tr, r.d, opt.gamma);
-        traverse(tr, r, tv);
+        traverse(tr, r, tv, stk);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = tv.C[ch] + (double)tv.T * (double)opt.bg[ch];
     }
-    traverse(tr, r, gv);
+    traverse(tr, r, gv, stk);
 }
 
 __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restrict__ rays, int64_t n, float gamma,
                                                int32_t max_leaves, int32_t* __restrict__ leaf_ids,
                                                int32_t* __restrict__ counts, int32_t* __restrict__ node_counts) {
+    PO_DECLARE_STACK(stk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float o[3], d[3];
@@ -292,13 +377,14 @@ __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restri
     for (int j = 0; j < max_leaves && ids; ++j) ids[j] = -1;
     TraceVisitor v{tr, 1.f, gamma, ids, ids ? max_leaves : 0, 0, 0};
     RayState r;
-    if (ray_setup(tr, o, d, r)) traverse(tr, r, v);
+    if (ray_setup(tr, o, d, r)) traverse(tr, r, v, stk);
     if (counts) counts[i] = v.count;
     if (node_counts) node_counts[i] = v.nodes;
 }
 
 __global__ void __launch_bounds__(256) k_stats(DevTree tr, const po_camera* __restrict__ cams, int W, int H,
                                                float gamma, unsigned long long* __restrict__ counters) {
+    PO_DECLARE_STACK(stk);
     int px, py;
     unsigned long long v4[4] = {0, 0, 0, 0};
     if (tile_pixel(W, H, px, py)) {
@@ -307,7 +393,7 @@ __global__ void __launch_bounds__(256) k_stats(DevTree tr, const po_camera* __re
         RayState r;
         if (ray_setup(tr, o, d, r)) {
             StatsVisitor v{tr, 1.f, gamma, 0, 0, 0};
-            traverse(tr, r, v);
+            traverse(tr, r, v, stk);
             v4[0] = v.leaves;
             v4[1] = v.sh_rows;
             v4[2] = v.nodes;
@@ -346,9 +432,10 @@ __global__ void __launch_bounds__(256) k_l2_loss(const float* __restrict__ pred,
 
 __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* __restrict__ sh, int32_t sh_row,
                                              int32_t ne, int64_t n_leaves, const float* __restrict__ grad_sigma,
-                                             const float* __restrict__ grad_sh, float lr) {
-    const int64_t total = n_leaves * (int64_t)(ne + 1);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+                                             const float* __restrict__ grad_sh, float lr, int64_t begin,
+                                             int64_t end) {
+    for (int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+         i += (int64_t)gridDim.x * blockDim.x) {
         if (i < n_leaves) {
             sigma[i] -= lr * grad_sigma[i];
         } else {
@@ -378,10 +465,40 @@ __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* _
 
 static inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
+template <class K>
+static int persistent_grid(K kernel, int64_t max_ctas) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    return (int)(g < max_ctas ? g : (max_ctas > 0 ? max_ctas : 1));
+}
+
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
-                          const RenderOpts& opt, float* out, cudaStream_t s) {
-    dim3 grid((W + 15) / 16, (H + 15) / 16, n_cams);
-    PO_DISPATCH(deg, f16, k_render<DEG, F16><<<grid, 256, 0, s>>>(tr, cams, W, H, opt, out));
+                          const RenderOpts& opt, float* out, unsigned* work, cudaStream_t s) {
+    const int64_t tiles = (int64_t)((W + 7) / 8) * ((H + 3) / 4) * n_cams;
+    if (tiles >= (int64_t)0xFFFFFFF0u) return cudaErrorInvalidValue;
+    // CTAs per SM the register budget is tuned for.  Default 2 (<= 128 registers): all 12
+    // LDG.128 of a leaf row stay in flight, which beat 3-4 CTAs/SM on B200 (r01: 4127 vs 3819
+    // vs 3160 FPS on c1).  PO_RENDER_MINB=1|2|3|4 selects another instance for experiments.
+    static const int minb = [] {
+        const char* e = getenv("PO_RENDER_MINB");
+        const int v = e ? atoi(e) : 2;
+        return (v >= 1 && v <= 4) ? v : 2;
+    }();
+    PO_DISPATCH(deg, f16, {
+        static int grid[5] = {0, 0, 0, 0, 0};   // per template instance; one device type per process
+        auto launch = [&](auto kern) {
+            if (grid[minb] == 0) grid[minb] = persistent_grid(kern, 1 << 30);
+            const int g = (int)((int64_t)grid[minb] < (tiles + 7) / 8 ? grid[minb] : (tiles + 7) / 8);
+            kern<<<g, 256, 0, s>>>(tr, cams, n_cams, W, H, opt, out, work);
+        };
+        if (minb == 1) launch(k_render<DEG, F16, 1>);
+        else if (minb == 2) launch(k_render<DEG, F16, 2>);
+        else if (minb == 3) launch(k_render<DEG, F16, 3>);
+        else launch(k_render<DEG, F16, 4>);
+    });
     return cudaGetLastError();
 }
 
@@ -429,12 +546,11 @@ cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, f
 }
 
 cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, const float* grad_sigma,
-                       const float* grad_sh, float lr, cudaStream_t s) {
-    const int64_t total = n_leaves * (int64_t)(ne + 1);
-    if (total == 0) return cudaSuccess;
-    unsigned g = grid1d(total, 256);
+                       const float* grad_sh, float lr, int64_t begin, int64_t end, cudaStream_t s) {
+    if (end <= begin) return cudaSuccess;
+    unsigned g = grid1d(end - begin, 256);
     if (g > 148 * 32) g = 148 * 32;
-    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr);
+    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr, begin, end);
     return cudaGetLastError();
 }
 

@@ -13,8 +13,10 @@ struct RenderOpts {
     float bg[3];
 };
 
+// work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
-                          const RenderOpts& opt, float* out, cudaStream_t s);
+                          const RenderOpts& opt, float* out, unsigned* work, cudaStream_t s);
+cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, float* rays, cudaStream_t s);
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
                                const RenderOpts& opt, float* out, double* aux, cudaStream_t s);
 cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
@@ -27,6 +29,6 @@ cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, i
 cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, float* dL_dC, double* loss,
                            cudaStream_t s);
 cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, const float* grad_sigma,
-                       const float* grad_sh, float lr, cudaStream_t s);
+                       const float* grad_sh, float lr, int64_t begin, int64_t end, cudaStream_t s);
 
 }  // namespace po

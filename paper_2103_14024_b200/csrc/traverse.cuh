@@ -46,9 +46,13 @@ struct RayState {
 
 // a1/a2: normalise d, move to grid units, slab-clip against [0, 2^D]^3.
 __device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], const float dir[3], RayState& r) {
-    float n2 = dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2];
-    if (!(n2 > 0.f) || !(n2 < INFINITY)) return false;
-    float rn = 1.0f / sqrtf(n2);
+    // scale by the largest component first so tiny / huge directions normalise without
+    // under- or overflow; a zero or non-finite direction renders the background
+    const float m = fmaxf(fabsf(dir[0]), fmaxf(fabsf(dir[1]), fabsf(dir[2])));
+    if (!(m >= 1.17549435e-38f) || !(m < INFINITY)) return false;   // zero / denormal / inf / NaN
+    const float im = 1.0f / m;
+    const float s0 = dir[0] * im, s1 = dir[1] * im, s2 = dir[2] * im;
+    const float rn = im / sqrtf(s0 * s0 + s1 * s1 + s2 * s2);
     const float G = (float)(1 << tr.depth);
     float tn = 0.f, tf = INFINITY;
 #pragma unroll
@@ -79,18 +83,28 @@ __device__ __forceinline__ int cell_of(float o, float dg, float t) {
     return dg < 0.f ? (int)ceilf(p) - 1 : (int)floorf(p);
 }
 
+// Per-thread ancestor stack in shared memory: slot L of thread t at base[L * kStackStride + t]
+// (consecutive lanes hit consecutive banks; no local-memory traffic).
+constexpr int kStackStride = 256;   // = threads per CTA of every kernel that traverses
+struct SmemStack {
+    uint32_t* base;
+    __device__ __forceinline__ uint32_t& operator[](int L) const { return base[L * kStackStride]; }
+};
+#define PO_DECLARE_STACK(name)                                                        \
+    __shared__ uint32_t name##_storage[(po::kMaxDepth + 1) * po::kStackStride];       \
+    po::SmemStack name{name##_storage + threadIdx.x}
+
 // a3: ordered descent.  Calls vis.on_node() for every internal node entered (root
 // included) and vis.on_leaf(idx, t_in, t_out) for every positive-length leaf segment in
 // ray order; traversal stops when on_leaf returns false (early stop) or the ray exits.
 template <class V>
-__device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V& vis) {
+__device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V& vis, const SmemStack& stk) {
     const int D = tr.depth;
     const int G = 1 << D;
     float t = r.tnear;
     int c[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) c[k] = min(max(cell_of(r.o[k], r.dg[k], t), 0), G - 1);
-    uint32_t stk[kMaxDepth + 1];
     stk[0] = 0u;
     int L = 0;
     vis.on_node();
@@ -101,47 +115,47 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         while (true) {
             shift = D - 1 - L;
             int oct = (((c[0] >> shift) & 1) << 2) | (((c[1] >> shift) & 1) << 1) | ((c[2] >> shift) & 1);
-            e = __ldg(tr.child + (size_t)node * 8 + oct);
+            e = __ldg(tr.child + (node * 8u + (uint32_t)oct));   // n_nodes <= 2^29 (checked at upload)
             if ((e >> 30) != kTagInternal) break;
             node = e & kIdxMask;
             ++L;
             stk[L] = node;
             vis.on_node();
         }
-        // the box of entry e: level L+1, 2^shift leaf cells per axis
+        // the box of entry e: level L+1, 2^shift leaf cells per axis.  Exit t per axis,
+        // branch-free: an axis with dg == 0 uses its upper face and inv = +inf, giving +inf
+        // (or NaN when the origin sits exactly on that face), which fminf ignores.
         const int size = 1 << shift;
         int lo[3];
-        float texit = INFINITY;
-        int ax = 0;
+        float te[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             lo[k] = c[k] & ~(size - 1);
-            if (r.dg[k] != 0.f) {
-                float face = (float)(r.dg[k] > 0.f ? lo[k] + size : lo[k]);
-                float te = (face - r.o[k]) * r.inv[k];
-                if (te < texit) {
-                    texit = te;
-                    ax = k;
-                }
-            }
+            const int face = (r.dg[k] >= 0.f) ? lo[k] + size : lo[k];
+            te[k] = ((float)face - r.o[k]) * r.inv[k];
         }
-        float tout = fminf(texit, r.tfar);
+        const float texit = fminf(fminf(te[0], te[1]), te[2]);
+        const int ax = (te[0] == texit) ? 0 : ((te[1] == texit) ? 1 : 2);   // first minimal axis
+        const float tout = fminf(texit, r.tfar);
         if ((e >> 30) == kTagLeaf && tout > t) {
             if (!vis.on_leaf(e & kIdxMask, t, tout)) return;
         }
         if (!(texit < r.tfar)) return;
         t = texit;
         int nc[3];
+        bool out = false;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            if (k == ax) {
-                nc[k] = r.dg[k] > 0.f ? lo[k] + size : lo[k] - 1;
-            } else {
-                nc[k] = min(max(cell_of(r.o[k], r.dg[k], t), lo[k]), lo[k] + size - 1);
-            }
+            // cell the ray enters on axis k: floor(p), or p-1 when moving down and p is integral
+            const float p = fmaf(t, r.dg[k], r.o[k]);
+            const float f = floorf(p);
+            const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
+            const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;   // exact on the exit axis
+            nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
+            out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
         }
-        if (nc[ax] < 0 || nc[ax] >= G) return;
-        int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
+        if (out) return;
+        const int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
         L = D - 1 - (31 - __clz(diff));
         c[0] = nc[0];
         c[1] = nc[1];

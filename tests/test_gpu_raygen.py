@@ -1,0 +1,52 @@
+"""a1 ray generation: po_camera_rays is the exact IEEE fp32 evaluation of the camera model
+(reading Q5), and po_render(cams) == po_render_rays(po_camera_rays(cams)) bit for bit."""
+import numpy as np
+import pytest
+
+import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+    import paper_2103_14024_b200 as po
+    return po, torch
+
+
+def _numpy_rays(cam, W, H):
+    """IEEE fp32 evaluation, same operation order as the header documents."""
+    f = np.float32
+    c = np.frombuffer(np.ascontiguousarray(cam).tobytes(), dtype=np.float32)[:16]
+    i = np.arange(W, dtype=np.float32)[None, :].repeat(H, 0)
+    j = np.arange(H, dtype=np.float32)[:, None].repeat(W, 1)
+    dx = ((i + f(0.5)) - c[14]) / c[12]
+    dy = -(((j + f(0.5)) - c[15]) / c[13])
+    d = [((c[k * 4] * dx) + (c[k * 4 + 1] * dy)) - c[k * 4 + 2] for k in range(3)]
+    o = [np.full_like(dx, c[k * 4 + 3]) for k in range(3)]
+    return np.stack(o + d, -1).astype(np.float32)
+
+
+def test_camera_rays_bit_exact(env):
+    po, torch = env
+    for cfg in ("c0", "c1"):
+        cam, W, H = gen.config_camera(cfg)
+        got = po.po_camera_rays(po.cams_tensor(cam), W, H)[0].cpu().numpy()
+        want = _numpy_rays(cam, W, H)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), cfg
+
+
+def test_render_equals_render_rays_of_camera_rays(env, c1_tree):
+    po, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    cams = np.concatenate([gen.config_camera("c1", v)[0] for v in range(3)])
+    ct = po.cams_tensor(cams)
+    img = po.po_render(tree, ct, 800, 800)
+    rays = po.po_camera_rays(ct, 800, 800).reshape(-1, 6)
+    img2 = po.po_render_rays(tree, rays).reshape(img.shape)
+    assert torch.equal(img, img2)
