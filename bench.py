@@ -274,6 +274,13 @@ def run_c4(args):
     for s in range(args.warmup + args.steps):
         rg = np.random.Generator(np.random.Philox(key=2 + s * ws + rank))
         pick = rg.choice(100 * W * H, size=n_rays, replace=False)
+        if not args.unsorted:
+            # batch preparation: order the sampled rays by (view, Morton(x, y)) so a warp's 32
+            # rays are spatially coherent (shared descent paths, fewer divergent branches)
+            view, p = pick // (W * H), pick % (W * H)
+            x, y = (p % W).astype(np.uint64), (p // W).astype(np.uint64)
+            mx = gen.trees._part1by2(x) | (gen.trees._part1by2(y) << np.uint64(1))
+            pick = pick[np.argsort((view.astype(np.uint64) << np.uint64(44)) | mx, kind="stable")]
         rays = torch.from_numpy(gen.camera_rays_f32(cams, W, H, pick // (W * H), pick % (W * H))).to(dev)
         tgt = po.po_render_rays(gt, rays, gamma=0.0)   # targets: renders of the unperturbed tree
         batches.append((rays, tgt))
@@ -409,6 +416,7 @@ def main():
     ap.add_argument("--workload", choices=["c1", "c4"], default="c1")
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
     ap.add_argument("--lr", type=float, default=1e-4, help="c4: SGD learning rate (loss is a sum over rays)")
+    ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -15,6 +15,9 @@ is part of the rendering method.
 """
 from __future__ import annotations
 
+import hashlib
+import os
+
 import numpy as np
 
 from .trees import Tree, build_from_leaf_cells, uniform_tree, random_tree
@@ -143,7 +146,7 @@ def _payload_c1(rng, cells, depth, sdf_vals, sh_degree=3, sigma_peak=768.0):
     sigma = sigma_peak / (1.0 + np.exp(2.0 * sdf_vals / h))
     neg = rng.random(n) < 0.05
     sigma[neg] = -np.abs(rng.normal(0.0, 10.0, int(neg.sum())))
-    sh = np.empty((n, B, 3))
+    sh = np.empty((n, B, 3), dtype=np.float32)
     omega = np.array([0.021, 0.017, 0.013])
     phase = cells.astype(np.float64) @ omega
     for ch, phi in enumerate((0.0, 2.0, 4.0)):
@@ -151,7 +154,7 @@ def _payload_c1(rng, cells, depth, sdf_vals, sh_degree=3, sigma_peak=768.0):
     b = 1
     for l in range(1, sh_degree + 1):
         nb = 2 * l + 1
-        sh[:, b:b + nb, :] = rng.normal(0.0, 0.8 / (l + 1), (n, nb, 3))
+        sh[:, b:b + nb, :] = rng.standard_normal((n, nb, 3), dtype=np.float32) * np.float32(0.8 / (l + 1))
         b += nb
     return sigma.astype(np.float32), sh.astype(np.float32)
 
@@ -173,8 +176,45 @@ def scene_c0(seed: int = 0) -> Tree:
                 np.full(cells.shape[0], depth, np.int32), cells)
 
 
+def _source_hash() -> str:
+    h = hashlib.sha1()
+    here = os.path.dirname(os.path.abspath(__file__))
+    for f in ("scenes.py", "trees.py"):
+        with open(os.path.join(here, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:12]
+
+
+def _cached(key: str, build):
+    """Disk cache of generated scenes (regenerated whenever missing or when gen/ changes), so
+    separate processes (tests, bench, smoke) do not each spend seconds-to-minutes in numpy."""
+    d = os.environ.get("PLENOCT_GEN_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "plenoct_gen"))
+    path = os.path.join(d, f"{key}_{_source_hash()}.npz")
+    if os.path.exists(path):
+        try:
+            z = np.load(path)
+            return Tree(int(z["depth"]), z["bbox_min"], float(z["edge"]), int(z["sh_degree"]), z["child"], z["sigma"],
+                        z["sh"], z["leaf_level"], z["leaf_cell"])
+        except Exception:
+            pass
+    t = build()
+    try:
+        os.makedirs(d, exist_ok=True)
+        tmp = path + f".tmp{os.getpid()}.npz"
+        np.savez(tmp, depth=t.depth, bbox_min=t.bbox_min, edge=t.edge, sh_degree=t.sh_degree, child=t.child,
+                 sigma=t.sigma, sh=t.sh, leaf_level=t.leaf_level, leaf_cell=t.leaf_cell)
+        os.replace(tmp, path)
+    except Exception:
+        pass
+    return t
+
+
 def scene_c1(seed: int = 0, thick: bool = False) -> Tree:
     """c1: NeRF-synthetic-shaped SDF object, depth-9 sparse octree, SH-3, fp32."""
+    return _cached(f"c1_s{seed}_t{int(thick)}", lambda: _scene_c1(seed, thick))
+
+
+def _scene_c1(seed: int, thick: bool) -> Tree:
     depth = 9
     lo = -8.0 if thick else -3.0
     cells = shell_cells(sdf_c1, depth, lo, 1.0)
@@ -189,6 +229,10 @@ def scene_c1(seed: int = 0, thick: bool = False) -> Tree:
 
 def scene_c3(seed: int = 0) -> Tree:
     """c3: Tanks&Temples-shaped bounded scene, depth-10 sparse octree, SH-3 (fp16 payload at upload)."""
+    return _cached(f"c3_s{seed}", lambda: _scene_c3(seed))
+
+
+def _scene_c3(seed: int) -> Tree:
     depth = 10
     cells = shell_cells(sdf_c3, depth, -3.0, 1.0)
     child, order = build_from_leaf_cells(cells, depth)

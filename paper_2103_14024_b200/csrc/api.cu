@@ -3,8 +3,11 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
+#include <cstdlib>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -27,6 +30,10 @@ struct po_tree {
     int cam_cap = 0;
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
+    // centre-out order of the 16x16 pixel blocks of a W x H view (built once per size)
+    unsigned* d_order = nullptr;
+    int order_w = 0, order_h = 0;
+    std::mutex order_mu;
     // work counters of the persistent render kernel: kWorkSlots pairs, handed out round
     // robin so up to kWorkSlots renders of one tree may be in flight on different streams
     static constexpr int kWorkSlots = 64;
@@ -70,6 +77,40 @@ struct DeviceGuard {
         if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
     }
 };
+
+// Block hand-out order for the persistent render: blocks sorted by the distance of their
+// centre from the image centre, so the costly on-object blocks of object-centred views go
+// first and the last claims (the tail of the launch) are cheap background blocks.
+// PO_RENDER_ORDER=raster disables it.  Returns NULL for raster order.
+const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_t* err) {
+    static const bool raster = [] {
+        const char* e = getenv("PO_RENDER_ORDER");
+        return e && std::strcmp(e, "raster") == 0;
+    }();
+    *err = cudaSuccess;
+    if (raster) return nullptr;
+    std::lock_guard<std::mutex> lk(t->order_mu);
+    if (t->d_order && t->order_w == W && t->order_h == H) return t->d_order;
+    const int bx = (W + 15) / 16, by = (H + 15) / 16;
+    std::vector<unsigned> ord((size_t)bx * by);
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = (unsigned)i;
+    const double cx = W * 0.5, cy = H * 0.5;
+    auto dist = [&](unsigned b) {
+        const double x = (b % bx) * 16.0 + 8.0 - cx, y = (b / bx) * 16.0 + 8.0 - cy;
+        return x * x + y * y;
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](unsigned a, unsigned b) { return dist(a) < dist(b); });
+    if ((*err = cudaStreamSynchronize(s)) != cudaSuccess) return nullptr;   // old table may be in use
+    if (t->d_order) cudaFree(t->d_order);
+    t->d_order = nullptr;
+    if ((*err = cudaMalloc(&t->d_order, ord.size() * sizeof(unsigned))) != cudaSuccess) return nullptr;
+    if ((*err = cudaMemcpy(t->d_order, ord.data(), ord.size() * sizeof(unsigned), cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+        return nullptr;
+    t->order_w = W;
+    t->order_h = H;
+    return t->d_order;
+}
 
 po::DevTree dev_tree(const po_tree* t) {
     po::DevTree d;
@@ -249,6 +290,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_cams) cudaFree(t->d_cams);
     if (t->d_work) cudaFree(t->d_work);
     if (t->d_img) cudaFree(t->d_img);
+    if (t->d_order) cudaFree(t->d_order);
     t->d_child = nullptr;
     delete t;
     return PO_OK;
@@ -317,8 +359,12 @@ po_status po_render(const po_tree* t, const po_camera* cams, int32_t n_cams, int
     if (!cams || !out_rgb) return fail(PO_ERR_INVALID_ARG, "cams / out_rgb NULL");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    po_tree* tm = const_cast<po_tree*>(t);   // only scratch (work counters, block order) is mutated
+    cudaError_t oe;
+    const unsigned* order = block_order(tm, W, H, (cudaStream_t)stream, &oe);
+    if (oe != cudaSuccess) return cuda_status(oe, "block order");
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
-                                      out_rgb, const_cast<po_tree*>(t)->next_work(), (cudaStream_t)stream),
+                                      out_rgb, tm->next_work(), order, (cudaStream_t)stream),
                     "po_render");
 }
 
@@ -356,8 +402,10 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
         if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(image)");
         t->img_cap = out_bytes;
     }
+    const unsigned* order = block_order(t, W, H, s, &e);
+    if (e != cudaSuccess) return cuda_status(e, "block order");
     po_status st = launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, t->d_cams,
-                                              n_cams, W, H, o, t->d_img, t->next_work(), s),
+                                              n_cams, W, H, o, t->d_img, t->next_work(), order, s),
                             "po_render_host");
     if (st == PO_OK) {
         e = cudaMemcpyAsync(out_host, t->d_img, out_bytes, cudaMemcpyDeviceToHost, s);

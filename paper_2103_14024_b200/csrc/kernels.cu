@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "kernels.h"
 #include "traverse.cuh"
@@ -219,10 +221,10 @@ __device__ __forceinline__ bool tile_pixel(int W, int H, int& px, int& py) {
 // across SMs with no tail wave.  The last CTA to finish resets the global counters
 // (work[0] = next block, work[1] = finished CTAs) for the next launch on the stream.
 constexpr int kSlotRing = 16;
-template <int DEG, bool F16, int MINB>
+template <int DEG, bool F16, int MINB, int OPT>
 __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camera* __restrict__ cams, int n_cams, int W,
                                                 int H, RenderOpts opt, float* __restrict__ out,
-                                                unsigned* __restrict__ work) {
+                                                unsigned* __restrict__ work, const unsigned* __restrict__ order) {
     PO_DECLARE_STACK(stk);
     __shared__ unsigned s_ticket;
     __shared__ unsigned s_block[kSlotRing];
@@ -255,7 +257,8 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         sub = __shfl_sync(0xffffffffu, sub, 0);
         if (blk >= total) break;
         const unsigned view = blk / per_view;
-        const unsigned rem = blk - view * per_view;
+        unsigned rem = blk - view * per_view;
+        if (order != nullptr) rem = __ldg(order + rem);   // centre-out block order (see launch_render)
         const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
         const int px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
         const int py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
             if (ray_setup(tr, o, d, r)) {
                 FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                traverse(tr, r, v, stk);
+                traverse<OPT>(tr, r, v, stk);
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
             }
@@ -476,29 +479,45 @@ static int persistent_grid(K kernel, int64_t max_ctas) {
 }
 
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
-                          const RenderOpts& opt, float* out, unsigned* work, cudaStream_t s) {
+                          const RenderOpts& opt, float* out, unsigned* work, const unsigned* order,
+                          cudaStream_t s) {
     const int64_t tiles = (int64_t)((W + 7) / 8) * ((H + 3) / 4) * n_cams;
     if (tiles >= (int64_t)0xFFFFFFF0u) return cudaErrorInvalidValue;
     // CTAs per SM the register budget is tuned for.  Default 2 (<= 128 registers): all 12
     // LDG.128 of a leaf row stay in flight, which beat 3-4 CTAs/SM on B200 (r01: 4127 vs 3819
-    // vs 3160 FPS on c1).  PO_RENDER_MINB=1|2|3|4 selects another instance for experiments.
+    // vs 3160 FPS on c1).  For the SH-3 fp32 path PO_RENDER_MINB=1..4 and PO_RENDER_OPT=0..3
+    // (traversal variants, traverse.cuh) select other instances for A/B experiments.
     static const int minb = [] {
         const char* e = getenv("PO_RENDER_MINB");
         const int v = e ? atoi(e) : 2;
         return (v >= 1 && v <= 4) ? v : 2;
     }();
-    PO_DISPATCH(deg, f16, {
-        static int grid[5] = {0, 0, 0, 0, 0};   // per template instance; one device type per process
-        auto launch = [&](auto kern) {
-            if (grid[minb] == 0) grid[minb] = persistent_grid(kern, 1 << 30);
-            const int g = (int)((int64_t)grid[minb] < (tiles + 7) / 8 ? grid[minb] : (tiles + 7) / 8);
-            kern<<<g, 256, 0, s>>>(tr, cams, n_cams, W, H, opt, out, work);
-        };
-        if (minb == 1) launch(k_render<DEG, F16, 1>);
-        else if (minb == 2) launch(k_render<DEG, F16, 2>);
-        else if (minb == 3) launch(k_render<DEG, F16, 3>);
-        else launch(k_render<DEG, F16, 4>);
-    });
+    static const int vopt = [] {
+        const char* e = getenv("PO_RENDER_OPT");
+        const int v = e ? atoi(e) : kOptDefault;
+        return (v >= 0 && v <= 3) ? v : kOptDefault;
+    }();
+    using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
+    KFn fn = nullptr;
+    if (deg == 3 && !f16) {
+#define PO_R3(M) {k_render<3, false, M, 0>, k_render<3, false, M, 1>, k_render<3, false, M, 2>, k_render<3, false, M, 3>}
+        static const KFn table[4][4] = {PO_R3(1), PO_R3(2), PO_R3(3), PO_R3(4)};
+#undef PO_R3
+        fn = table[minb - 1][vopt];
+    } else {
+        PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kOptDefault>);
+    }
+    static std::mutex mu;
+    static std::map<KFn, int> grids;   // persistent grid size per kernel instance
+    int grid;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = grids.find(fn);
+        if (it == grids.end()) it = grids.emplace(fn, persistent_grid(fn, 1 << 30)).first;
+        grid = it->second;
+    }
+    const int g = (int)((int64_t)grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8);
+    fn<<<g, 256, 0, s>>>(tr, cams, n_cams, W, H, opt, out, work, order);
     return cudaGetLastError();
 }
 

@@ -14,8 +14,11 @@ struct RenderOpts {
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.
+// order: NULL (raster) or a device permutation of the ceil(W/16)*ceil(H/16) blocks of a view
+// giving the order in which blocks are handed out.
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
-                          const RenderOpts& opt, float* out, unsigned* work, cudaStream_t s);
+                          const RenderOpts& opt, float* out, unsigned* work, const unsigned* order,
+                          cudaStream_t s);
 cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, float* rays, cudaStream_t s);
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
                                const RenderOpts& opt, float* out, double* aux, cudaStream_t s);

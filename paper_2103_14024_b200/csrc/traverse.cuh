@@ -97,7 +97,13 @@ struct SmemStack {
 // a3: ordered descent.  Calls vis.on_node() for every internal node entered (root
 // included) and vis.on_leaf(idx, t_in, t_out) for every positive-length leaf segment in
 // ray order; traversal stops when on_leaf returns false (early stop) or the ray exits.
-template <class V>
+// Traversal variants (compile time, selected by measurement; see kernels.cu launch_render):
+//   kOptParentCache  register copy of the current level-(D-1) node's 8 child entries
+//   kOptLeafStep     fast neighbour step when the box is a single leaf-level cell
+constexpr int kOptParentCache = 1, kOptLeafStep = 2;
+constexpr int kOptDefault = 0;
+
+template <int OPT = kOptDefault, class V>
 __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V& vis, const SmemStack& stk) {
     const int D = tr.depth;
     const int G = 1 << D;
@@ -108,6 +114,12 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     stk[0] = 0u;
     int L = 0;
     vis.on_node();
+    // Register copy of the 8 child entries of the last node entered at level D-1 (the parents
+    // of leaf-level cells): one 32-B sector read by two LDG.128 when the ray enters such a
+    // node, after which stepping between its 2x2x2 cells needs no memory access at all.
+    uint32_t pnode = 0xFFFFFFFFu;
+    uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
+    const uint4* __restrict__ child4 = reinterpret_cast<const uint4*>(tr.child);
     while (true) {
         uint32_t node = stk[L];
         uint32_t e;
@@ -115,7 +127,18 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         while (true) {
             shift = D - 1 - L;
             int oct = (((c[0] >> shift) & 1) << 2) | (((c[1] >> shift) & 1) << 1) | ((c[2] >> shift) & 1);
-            e = __ldg(tr.child + (node * 8u + (uint32_t)oct));   // n_nodes <= 2^29 (checked at upload)
+            if ((OPT & kOptParentCache) && shift == 0) {
+                if (node != pnode) {
+                    pa = __ldg(child4 + 2u * node);
+                    pb = __ldg(child4 + 2u * node + 1u);
+                    pnode = node;
+                }
+                const uint4 h = (oct & 4) ? pb : pa;
+                const uint32_t x0 = (oct & 1) ? h.y : h.x, x1 = (oct & 1) ? h.w : h.z;
+                e = (oct & 2) ? x1 : x0;
+            } else {
+                e = __ldg(tr.child + (node * 8u + (uint32_t)oct));   // n_nodes <= 2^29 (checked at upload)
+            }
             if ((e >> 30) != kTagInternal) break;
             node = e & kIdxMask;
             ++L;
@@ -144,15 +167,25 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         t = texit;
         int nc[3];
         bool out = false;
+        if ((OPT & kOptLeafStep) && size == 1) {
+            // leaf-level box (the common step): the other two coordinates cannot change
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            // cell the ray enters on axis k: floor(p), or p-1 when moving down and p is integral
-            const float p = fmaf(t, r.dg[k], r.o[k]);
-            const float f = floorf(p);
-            const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
-            const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;   // exact on the exit axis
-            nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
-            out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
+            for (int k = 0; k < 3; ++k) {
+                const int nex = c[k] + ((r.dg[k] > 0.f) ? 1 : -1);
+                nc[k] = (k == ax) ? nex : c[k];
+                out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                // cell the ray enters on axis k: floor(p), or p-1 when moving down and p is integral
+                const float p = fmaf(t, r.dg[k], r.o[k]);
+                const float f = floorf(p);
+                const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
+                const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;   // exact on the exit axis
+                nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
+                out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
+            }
         }
         if (out) return;
         const int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
@@ -242,7 +275,14 @@ __device__ __forceinline__ void sh_dot(const DevTree& tr, uint32_t idx, const fl
     }
 }
 
-__device__ __forceinline__ float sigmoidf_(float z) { return __fdividef(1.0f, 1.0f + __expf(-z)); }
+// e^x as one MUFU.EX2 (flush-to-zero: results below 2^-126 become 0, harmless for T and colours)
+__device__ __forceinline__ float exp_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(x, 1.44269504088896341f)));
+    return y;
+}
+
+__device__ __forceinline__ float sigmoidf_(float z) { return __fdividef(1.0f, 1.0f + exp_ftz(-z)); }
 
 // a4: e = exp(-sigma delta), weight w = T (1 - e), T' = T e.  Explicit _rn intrinsics so
 // every kernel that evaluates a leaf produces bit-identical w, T' (forward, trace,
@@ -252,7 +292,7 @@ struct Absorb {
 };
 __device__ __forceinline__ Absorb absorb(float T, float sigma, float delta) {
     Absorb a;
-    a.e = __expf(-__fmul_rn(sigma, delta));
+    a.e = exp_ftz(-__fmul_rn(sigma, delta));
     a.w = __fmul_rn(T, __fsub_rn(1.0f, a.e));
     a.Tn = __fmul_rn(T, a.e);
     return a;
