@@ -110,7 +110,14 @@ def _dist():
     return ws, rank, local
 
 
-def _workload_desc(tree_gen):
+def _workload_desc(tree_gen, wl="c1"):
+    if wl == "c3":
+        return {"workload": "c3: Tanks&Temples-shaped bounded scene, depth-10 sparse octree (1024^3), "
+                            f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp16 payload (sigma fp32), "
+                            "1920x1080, gamma 0.01",
+                "views": "orbit r 2.6, el 15 deg, az = 20 + 1.8*i deg, f 1400 px; rank r renders views r, r+N, ...",
+                "l2": "flushed (256 MiB write) before every timed step; only the render is inside the CUDA events",
+                "global_batch": "1 frame per rank per step"}
     return {"workload": "c1: NeRF-synthetic-shaped SDF object, depth-9 sparse octree (512^3), "
                         f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp32 payload, 800x800, gamma 0.01",
             "views": "c1 orbit, az = 37 + 1.8*i deg, el 30 deg, r 3.4, f 1111.1 px; rank r renders views r, r+N, ...",
@@ -124,6 +131,10 @@ def run_ours(args):
     import gen
     import paper_2103_14024_b200 as po
 
+    wl = args.workload
+    W, H = (1920, 1080) if wl == "c3" else (800, 800)
+    payload = po.PO_F16 if wl == "c3" else po.PO_F32
+    metric = "1920x1080 FPS, SH-3 depth-10 fp16 PlenOctree (c3)" if wl == "c3" else METRIC
     ws, rank, local = _dist()
     if ws > 1:
         import torch.distributed as dist
@@ -132,10 +143,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     po.lib()
-    t_gen = gen.scene_c1()
-    tree = po.tree_from_gen(t_gen, device=local)
+    t_gen = gen.scene_c3() if wl == "c3" else gen.scene_c1()
+    tree = po.tree_from_gen(t_gen, payload=payload, device=local)
     n_views = max(args.steps + args.warmup, 1) * ws
-    cam_recs = np.concatenate([gen.config_camera("c1", v)[0] for v in range(n_views)])
+    cam_recs = np.concatenate([gen.config_camera(wl, v)[0] for v in range(n_views)])
     cams = po.cams_tensor(cam_recs, dev)
     out = torch.empty((1, H, W, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -146,7 +157,7 @@ def run_ours(args):
 
     # algorithmic bytes per launch: counters of the same traversal
     B = t_gen.basis_dim
-    row_bytes = 3 * B * 4
+    row_bytes = 3 * B * (2 if payload == po.PO_F16 else 4)
     stats = {"leaf_visits": 0, "sh_rows": 0, "nodes": 0, "hit_rays": 0}
     for s in range(args.warmup, args.warmup + args.steps):
         v = view_of(s)
@@ -219,26 +230,27 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = _peaks()
         achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-        traffic, tsrc = _ncu_traffic()
+        traffic, tsrc = _ncu_traffic() if wl == "c1" else (None, None)
         line = {
-            "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": metric, "value": round(fps, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural SDF scene, seeded)",
-            "config": _workload_desc(t_gen) | {"parallelism": f"view-sharded x{ws}, tree replicated"},
+            "config": _workload_desc(t_gen, wl) | {"parallelism": f"view-sharded x{ws}, tree replicated"},
             "mrays_per_s": round(fps * W * H / 1e6, 1),
             "leaf_visits_per_frame": stats["leaf_visits"] / K,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "po::k_render<3,false>", "peak_source": peak_src,
+                         "kernel": f"po::k_render<3,{int(payload == po.PO_F16)}>", "peak_source": peak_src,
                          "alg_bytes_per_launch": round(alg_bytes),
-                         "alg_bytes_def": "leaf visits*4 B sigma + SH rows*192 B + internal nodes met*32 B + 12 B/pixel out",
+                         "alg_bytes_def": f"leaf visits*4 B sigma + SH rows*{row_bytes} B + internal nodes met*32 B "
+                                          "+ 12 B/pixel out",
                          "traffic_source": tsrc},
             "e2e": {"value": round(e2e_fps, 2), "unit": UNIT, "h2d_bytes_per_step": 64,
                     "d2h_bytes_per_step": W * H * 12, "entry": "po_render_host (host cameras -> host image)"},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
-        if not args.no_cpu_baseline and ws == 1:
+        if not args.no_cpu_baseline and ws == 1 and wl == "c1":
             line["cpu_baseline"] = cpu_baseline(t_gen, seconds=args.cpu_seconds)
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -413,7 +425,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c1", "c4"], default="c1")
+    ap.add_argument("--workload", choices=["c1", "c3", "c4"], default="c1")
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
     ap.add_argument("--lr", type=float, default=1e-4, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")

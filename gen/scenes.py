@@ -96,32 +96,35 @@ def sdf_c3(p):
 
 
 def shell_cells(sdf, depth: int, lo_h: float = -3.0, hi_h: float = 1.0, lip: float = 1.6,
-                start_level: int = 3, chunk: int = 1 << 22):
+                start_level: int = 3, chunk: int = 1 << 20):
     """Leaf cells at ``depth`` whose centre SDF / h lies in the open interval (lo_h, hi_h).
 
     Coarse-to-fine: a level-L cell is refined only if its centre value could
-    reach the band given a Lipschitz bound ``lip`` on the SDF.
+    reach the band given a Lipschitz bound ``lip`` on the SDF.  Chunks are evaluated on a
+    thread pool (numpy releases the GIL); the result does not depend on the thread count.
     """
+    from concurrent.futures import ThreadPoolExecutor
     h = EDGE / (1 << depth)
     r = np.arange(1 << start_level, dtype=np.int64)
     cells = np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3)
     offs = np.array([[(o >> 2) & 1, (o >> 1) & 1, o & 1] for o in range(8)], dtype=np.int64)
-    for L in range(start_level, depth + 1):
-        size = EDGE / (1 << L)
-        keep_parts = []
-        for s in range(0, cells.shape[0], chunk):
-            c = cells[s:s + chunk]
-            centre = BBOX_MIN.astype(np.float64) + (c + 0.5) * size
-            f = sdf(centre)
-            if L == depth:
-                m = (f / h > lo_h) & (f / h < hi_h)
-            else:
-                reach = lip * np.sqrt(3.0) * size * 0.5
-                m = (f - reach < hi_h * h) & (f + reach > lo_h * h)
-            keep_parts.append(c[m])
-        cells = np.concatenate(keep_parts) if keep_parts else np.zeros((0, 3), np.int64)
-        if L < depth:
-            cells = (cells[:, None, :] * 2 + offs[None]).reshape(-1, 3)
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as pool:
+        for L in range(start_level, depth + 1):
+            size = EDGE / (1 << L)
+
+            def keep(c, L=L, size=size):
+                centre = BBOX_MIN.astype(np.float64) + (c + 0.5) * size
+                f = sdf(centre)
+                if L == depth:
+                    m = (f / h > lo_h) & (f / h < hi_h)
+                else:
+                    reach = lip * np.sqrt(3.0) * size * 0.5
+                    m = (f - reach < hi_h * h) & (f + reach > lo_h * h)
+                return c[m]
+            parts = list(pool.map(keep, [cells[s:s + chunk] for s in range(0, cells.shape[0], chunk)]))
+            cells = np.concatenate(parts) if parts else np.zeros((0, 3), np.int64)
+            if L < depth:
+                cells = (cells[:, None, :] * 2 + offs[None]).reshape(-1, 3)
     return cells
 
 

@@ -289,6 +289,127 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
     }
 }
 
+// Lane-refill variant of k_render (dynamic ray fetch): every lane of a warp owns one ray at a
+// time and the warp advances all its rays by one box per iteration; lanes whose ray finished
+// take the next pixels of the warp's current 8x4 tile (a new tile is claimed through the same
+// CTA-slot scheme when it runs out) as soon as at least `refill_min` lanes are idle.  This keeps
+// the SIMT lanes busy instead of letting 31 lanes wait for the longest ray of the tile.
+template <int DEG, bool F16, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_render_refill(DevTree tr, const po_camera* __restrict__ cams,
+                                                             int n_cams, int W, int H, RenderOpts opt,
+                                                             float* __restrict__ out, unsigned* __restrict__ work,
+                                                             const unsigned* __restrict__ order, int refill_min) {
+    PO_DECLARE_STACK(stk);
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_block[kSlotRing];
+    __shared__ volatile unsigned s_pub[kSlotRing];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (threadIdx.x == 0) s_ticket = 0;
+    if (threadIdx.x < kSlotRing) s_pub[threadIdx.x] = 0xFFFFFFFFu;
+    __syncthreads();
+    const unsigned bx_n = (unsigned)(W + 15) >> 4, by_n = (unsigned)(H + 15) >> 4;
+    const unsigned per_view = bx_n * by_n;
+    const unsigned total = per_view * (unsigned)n_cams;
+    // warp-uniform queue: the current 8x4 tile and how many of its 32 pixels were handed out
+    int q_x0 = 0, q_y0 = 0, q_view = 0, q_next = 32;
+    bool more = true;
+    // lane state
+    bool active = false;
+    int px = 0, py = 0, pview = 0;
+    RayState r;
+    TravState ts;
+    const float d0[3] = {0.f, 0.f, 1.f};
+    FwdVisitor<DEG, F16> v(tr, d0, opt.gamma);   // Y, T, C are re-initialised at every refill
+    while (true) {
+        unsigned idle = __ballot_sync(0xffffffffu, !active);
+        if (more && idle != 0u && (__popc(idle) >= refill_min || idle == 0xffffffffu)) {
+            while (more && idle != 0u) {
+                if (q_next == 32) {   // claim a new tile (warp-uniform)
+                    unsigned blk = 0, sub = 0;
+                    if (lane == 0) {
+                        const unsigned k = atomicAdd(&s_ticket, 1u);
+                        const unsigned slot = k >> 3;
+                        sub = k & 7u;
+                        if (sub == 0) {
+                            s_block[slot % kSlotRing] = atomicAdd(work, 1u);
+                            __threadfence_block();
+                            s_pub[slot % kSlotRing] = slot;
+                        } else {
+                            while (s_pub[slot % kSlotRing] != slot) {
+                            }
+                            __threadfence_block();
+                        }
+                        blk = s_block[slot % kSlotRing];
+                    }
+                    blk = __shfl_sync(0xffffffffu, blk, 0);
+                    sub = __shfl_sync(0xffffffffu, sub, 0);
+                    if (blk >= total) {
+                        more = false;
+                        break;
+                    }
+                    q_view = (int)(blk / per_view);
+                    unsigned rem = blk - (unsigned)q_view * per_view;
+                    if (order != nullptr) rem = __ldg(order + rem);
+                    const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
+                    q_x0 = bx * 16 + (int)(sub & 1u) * 8;
+                    q_y0 = by * 16 + (int)(sub >> 1) * 4;
+                    q_next = 0;
+                }
+                const int rank = __popc(idle & lt_mask);
+                const int take = min(32 - q_next, __popc(idle));
+                bool got = false;
+                if (!active && rank < take) {
+                    const int slot = q_next + rank;
+                    px = q_x0 + (slot & 7);
+                    py = q_y0 + (slot >> 3);
+                    pview = q_view;
+                    if (px < W && py < H) {
+                        float o[3], d[3];
+                        camera_ray(cams, pview, px, py, o, d);
+                        if (ray_setup(tr, o, d, r)) {
+                            sh_basis<DEG>(r.d, tr.odd_sign, v.Y);
+                            v.T = 1.f;
+                            v.C[0] = v.C[1] = v.C[2] = 0.f;
+                            trav_begin(tr, r, ts, stk);
+                            got = true;
+                        } else {
+                            float* p = out + (((size_t)pview * H + py) * W + px) * 3;
+                            p[0] = opt.bg[0];
+                            p[1] = opt.bg[1];
+                            p[2] = opt.bg[2];
+                        }
+                    }
+                }
+                active = active || got;
+                q_next += take;
+                idle = __ballot_sync(0xffffffffu, !active);
+            }
+        }
+        if (__ballot_sync(0xffffffffu, active) == 0u) {
+            if (!more) break;
+            continue;
+        }
+        if (active) {
+            if (!trav_step(tr, r, ts, v, stk)) {
+                active = false;
+                float* p = out + (((size_t)pview * H + py) * W + px) * 3;
+                p[0] = fmaf(v.T, opt.bg[0], v.C[0]);
+                p[1] = fmaf(v.T, opt.bg[1], v.C[1]);
+                p[2] = fmaf(v.T, opt.bg[2], v.C[2]);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            atomicExch(work, 0u);
+            atomicExch(work + 1, 0u);
+        }
+    }
+}
+
 template <int DEG, bool F16>
 __global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                      RenderOpts opt, float* __restrict__ out, double* __restrict__ aux) {
@@ -497,6 +618,30 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
         const int v = e ? atoi(e) : kOptDefault;
         return (v >= 0 && v <= 3) ? v : kOptDefault;
     }();
+    static const int refill_min = [] {
+        const char* e = getenv("PO_RENDER_REFILL");
+        const int v = e ? atoi(e) : 0;
+        return (v >= 0 && v <= 32) ? v : 0;
+    }();
+    if (refill_min > 0 && deg == 3 && !f16) {
+        using RFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
+                             int);
+        static const RFn rt[4] = {k_render_refill<3, false, 1>, k_render_refill<3, false, 2>,
+                                  k_render_refill<3, false, 3>, k_render_refill<3, false, 4>};
+        RFn rf = rt[minb - 1];
+        static std::mutex rmu;
+        static std::map<RFn, int> rgrids;
+        int grid;
+        {
+            std::lock_guard<std::mutex> lk(rmu);
+            auto it = rgrids.find(rf);
+            if (it == rgrids.end()) it = rgrids.emplace(rf, persistent_grid(rf, 1 << 30)).first;
+            grid = it->second;
+        }
+        const int g = (int)((int64_t)grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8);
+        rf<<<g, 256, 0, s>>>(tr, cams, n_cams, W, H, opt, out, work, order, refill_min);
+        return cudaGetLastError();
+    }
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
     KFn fn = nullptr;
     if (deg == 3 && !f16) {

@@ -196,6 +196,81 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     }
 }
 
+// Resumable form of the same traversal (identical arithmetic, one box per call), for kernels
+// that refill finished lanes with new rays between steps.
+struct TravState {
+    float t;
+    int c[3];
+    int L;
+};
+
+__device__ __forceinline__ void trav_begin(const DevTree& tr, const RayState& r, TravState& s, const SmemStack& stk) {
+    const int G = 1 << tr.depth;
+    s.t = r.tnear;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s.c[k] = min(max(cell_of(r.o[k], r.dg[k], s.t), 0), G - 1);
+    stk[0] = 0u;
+    s.L = 0;
+}
+
+// One box: descend to the entry containing the current cell, visit it if it is a leaf,
+// advance to the next cell.  Returns false once the ray is finished.
+template <class V>
+__device__ __forceinline__ bool trav_step(const DevTree& tr, const RayState& r, TravState& s, V& vis,
+                                          const SmemStack& stk) {
+    const int D = tr.depth;
+    const int G = 1 << D;
+    int L = s.L;
+    uint32_t node = stk[L];
+    uint32_t e;
+    int shift;
+    while (true) {
+        shift = D - 1 - L;
+        const int oct = (((s.c[0] >> shift) & 1) << 2) | (((s.c[1] >> shift) & 1) << 1) | ((s.c[2] >> shift) & 1);
+        e = __ldg(tr.child + (node * 8u + (uint32_t)oct));
+        if ((e >> 30) != kTagInternal) break;
+        node = e & kIdxMask;
+        ++L;
+        stk[L] = node;
+        vis.on_node();
+    }
+    const int size = 1 << shift;
+    int lo[3];
+    float te[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = s.c[k] & ~(size - 1);
+        const int face = (r.dg[k] >= 0.f) ? lo[k] + size : lo[k];
+        te[k] = ((float)face - r.o[k]) * r.inv[k];
+    }
+    const float texit = fminf(fminf(te[0], te[1]), te[2]);
+    const int ax = (te[0] == texit) ? 0 : ((te[1] == texit) ? 1 : 2);
+    const float tout = fminf(texit, r.tfar);
+    if ((e >> 30) == kTagLeaf && tout > s.t) {
+        if (!vis.on_leaf(e & kIdxMask, s.t, tout)) return false;
+    }
+    if (!(texit < r.tfar)) return false;
+    s.t = texit;
+    int nc[3];
+    bool out = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float p = fmaf(s.t, r.dg[k], r.o[k]);
+        const float f = floorf(p);
+        const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
+        const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;
+        nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
+        out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
+    }
+    if (out) return false;
+    const int diff = (s.c[0] ^ nc[0]) | (s.c[1] ^ nc[1]) | (s.c[2] ^ nc[2]);
+    s.L = D - 1 - (31 - __clz(diff));
+    s.c[0] = nc[0];
+    s.c[1] = nc[1];
+    s.c[2] = nc[2];
+    return true;
+}
+
 // ---------------------------------------------------------------------------------
 // a5: real SH basis, l <= 3, Cartesian form of App. B.1 under the
 // Condon-Shortley reading (Q16); odd-|m| functions are multiplied by odd_sign.
