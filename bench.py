@@ -180,10 +180,11 @@ def run_ours(args):
     l0 = po.launch_count()
     evs = []
     for s in range(args.warmup, args.warmup + args.steps):
-        flush.zero_()
+        if args.l2 == "flush":
+            flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        v = view_of(s)
+        v = view_of(s) if args.l2 != "same" else view_of(args.warmup)
         e0.record(stream)
         po.po_render(tree, cams[v:v + 1], W, H, out=out, gamma=GAMMA)
         e1.record(stream)
@@ -235,7 +236,8 @@ def run_ours(args):
             "metric": metric, "value": round(fps, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural SDF scene, seeded)",
-            "config": _workload_desc(t_gen, wl) | {"parallelism": f"view-sharded x{ws}, tree replicated"},
+            "config": _workload_desc(t_gen, wl) | {"parallelism": f"view-sharded x{ws}, tree replicated"}
+                      | ({"l2": f"NOT flushed ({args.l2}): analysis only"} if args.l2 != "flush" else {}),
             "mrays_per_s": round(fps * W * H / 1e6, 1),
             "leaf_visits_per_frame": stats["leaf_visits"] / K,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -285,8 +287,20 @@ def run_c4(args):
     batches = []
     for s in range(args.warmup + args.steps):
         rg = np.random.Generator(np.random.Philox(key=2 + s * ws + rank))
-        pick = rg.choice(100 * W * H, size=n_rays, replace=False)
-        if not args.unsorted:
+        if args.ray_sampling == "tile":
+            # sample 8x4-pixel tiles without replacement (each pixel still at most once per
+            # batch); a tile's 32 rays are consecutive, i.e. one coherent warp
+            tx_n, ty_n = W // 8, H // 4
+            tiles = rg.choice(100 * tx_n * ty_n, size=n_rays // 32, replace=False)
+            tiles.sort()
+            tv, tr_ = tiles // (tx_n * ty_n), tiles % (tx_n * ty_n)
+            x0, y0 = (tr_ % tx_n) * 8, (tr_ // tx_n) * 4
+            lane = np.arange(32)
+            pix = (y0[:, None] + lane[None] // 8) * W + x0[:, None] + lane[None] % 8
+            pick = (tv[:, None] * (W * H) + pix).reshape(-1)
+        else:
+            pick = rg.choice(100 * W * H, size=n_rays, replace=False)
+        if args.ray_sampling == "pixel" and not args.unsorted:
             # batch preparation: order the sampled rays by (view, Morton(x, y)) so a warp's 32
             # rays are spatially coherent (shared descent paths, fewer divergent branches)
             view, p = pick // (W * H), pick % (W * H)
@@ -345,7 +359,9 @@ def run_c4(args):
             "dtype": "f32", "data": "synthetic (c1 tree perturbed; targets = renders of the unperturbed tree)",
             "config": {"workload": f"c4: {n_rays} rays per GPU per step from 100 Fibonacci-hemisphere 800x800 views, "
                                    "gamma 0, SGD lr %g" % args.lr, "parallelism": f"ray data-parallel x{ws}, "
-                                   "tree replicated, bucketed NCCL SUM allreduce"},
+                                   "tree replicated, bucketed NCCL SUM allreduce",
+                       "ray_sampling": args.ray_sampling + ("" if args.ray_sampling == "tile" or not args.unsorted
+                                                           else " (unsorted)")},
             "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
             "leaf_visits_per_step": visits / K,
             "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
@@ -426,9 +442,14 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["c1", "c3", "c4"], default="c1")
+    ap.add_argument("--l2", choices=["flush", "orbit", "same"], default="flush",
+                    help="analysis only: 'orbit' = consecutive orbit views without flushing (warm, realistic "
+                         "frame-to-frame reuse), 'same' = one view repeated; the reported number uses 'flush'")
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
-    ap.add_argument("--lr", type=float, default=1e-4, help="c4: SGD learning rate (loss is a sum over rays)")
+    ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
+    ap.add_argument("--ray-sampling", choices=["tile", "pixel"], default="tile",
+                    help="c4: sample 8x4 pixel tiles (coherent warps) or single pixels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -45,6 +45,69 @@ struct FwdVisitor {
     }
 };
 
+// Forward visitor whose leaf rows land in shared memory through cp.async (LDGSTS) instead of
+// 48 registers: the row loads stay fully in flight while the kernel fits 3 CTAs (24 warps)
+// per SM instead of 2.  Each thread owns a 208-B slot (52 words: conflict-free LDS.128).
+constexpr int kStageWords = 52;
+template <int DEG, bool F16>
+struct FwdVisitorSm {
+    const DevTree& tr;
+    float Y[ShDim<DEG>::B];
+    float T, gamma;
+    float C[3];
+    float* stage;   // this thread's slot
+    __device__ FwdVisitorSm(const DevTree& t, const float d[3], float g, float* st)
+        : tr(t), T(1.f), gamma(g), stage(st) {
+        sh_basis<DEG>(d, t.odd_sign, Y);
+        C[0] = C[1] = C[2] = 0.f;
+    }
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        constexpr int NE = 3 * ShDim<DEG>::B;
+        constexpr int NB = F16 ? (NE * 2 + 15) / 16 : (NE * 4 + 15) / 16;   // 16-B chunks per row
+        const char* src = static_cast<const char*>(tr.sh) + (size_t)idx * tr.sh_row * (F16 ? 2 : 4);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage);
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * j), "l"(src + 16 * j) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const float st = __ldg(tr.sigma + idx);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (!(st > 0.f)) return true;
+        float z[3] = {0.f, 0.f, 0.f};
+        if (!F16) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const float4 v = *reinterpret_cast<const float4*>(stage + 4 * j);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int el = 4 * j + q;
+                    if (el < NE) z[el % 3] = fmaf(vv[q], Y[el / 3], z[el % 3]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const uint4 v = *reinterpret_cast<const uint4*>(stage + 4 * j);
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[q]));
+                    const int el0 = 8 * j + 2 * q, el1 = el0 + 1;
+                    if (el0 < NE) z[el0 % 3] = fmaf(f.x, Y[el0 / 3], z[el0 % 3]);
+                    if (el1 < NE) z[el1 % 3] = fmaf(f.y, Y[el1 / 3], z[el1 % 3]);
+                }
+            }
+        }
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(a.w, sigmoidf_(z[ch]), C[ch]);
+        T = a.Tn;
+        return !(T < gamma);
+    }
+};
+
 // Forward with the colour sum accumulated in double (pass 1 of the backward).
 template <int DEG, bool F16>
 struct TotalVisitor {
@@ -268,136 +331,23 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             RayState r;
             float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
             if (ray_setup(tr, o, d, r)) {
-                FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                traverse<OPT>(tr, r, v, stk);
+                if constexpr ((OPT & kOptSmemRow) != 0) {
+                    extern __shared__ __align__(16) float po_dyn_smem[];
+                    FwdVisitorSm<DEG, F16> v(tr, r.d, opt.gamma, po_dyn_smem + threadIdx.x * kStageWords);
+                    traverse<OPT & 3>(tr, r, v, stk);
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+                    for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+                } else {
+                    FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
+                    traverse<OPT & 3>(tr, r, v, stk);
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+                }
             }
             float* p = out + (((size_t)view * H + py) * W + px) * 3;
             p[0] = C[0];
             p[1] = C[1];
             p[2] = C[2];
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
-            atomicExch(work, 0u);
-            atomicExch(work + 1, 0u);
-        }
-    }
-}
-
-// Lane-refill variant of k_render (dynamic ray fetch): every lane of a warp owns one ray at a
-// time and the warp advances all its rays by one box per iteration; lanes whose ray finished
-// take the next pixels of the warp's current 8x4 tile (a new tile is claimed through the same
-// CTA-slot scheme when it runs out) as soon as at least `refill_min` lanes are idle.  This keeps
-// the SIMT lanes busy instead of letting 31 lanes wait for the longest ray of the tile.
-template <int DEG, bool F16, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_render_refill(DevTree tr, const po_camera* __restrict__ cams,
-                                                             int n_cams, int W, int H, RenderOpts opt,
-                                                             float* __restrict__ out, unsigned* __restrict__ work,
-                                                             const unsigned* __restrict__ order, int refill_min) {
-    PO_DECLARE_STACK(stk);
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned s_block[kSlotRing];
-    __shared__ volatile unsigned s_pub[kSlotRing];
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    if (threadIdx.x == 0) s_ticket = 0;
-    if (threadIdx.x < kSlotRing) s_pub[threadIdx.x] = 0xFFFFFFFFu;
-    __syncthreads();
-    const unsigned bx_n = (unsigned)(W + 15) >> 4, by_n = (unsigned)(H + 15) >> 4;
-    const unsigned per_view = bx_n * by_n;
-    const unsigned total = per_view * (unsigned)n_cams;
-    // warp-uniform queue: the current 8x4 tile and how many of its 32 pixels were handed out
-    int q_x0 = 0, q_y0 = 0, q_view = 0, q_next = 32;
-    bool more = true;
-    // lane state
-    bool active = false;
-    int px = 0, py = 0, pview = 0;
-    RayState r;
-    TravState ts;
-    const float d0[3] = {0.f, 0.f, 1.f};
-    FwdVisitor<DEG, F16> v(tr, d0, opt.gamma);   // Y, T, C are re-initialised at every refill
-    while (true) {
-        unsigned idle = __ballot_sync(0xffffffffu, !active);
-        if (more && idle != 0u && (__popc(idle) >= refill_min || idle == 0xffffffffu)) {
-            while (more && idle != 0u) {
-                if (q_next == 32) {   // claim a new tile (warp-uniform)
-                    unsigned blk = 0, sub = 0;
-                    if (lane == 0) {
-                        const unsigned k = atomicAdd(&s_ticket, 1u);
-                        const unsigned slot = k >> 3;
-                        sub = k & 7u;
-                        if (sub == 0) {
-                            s_block[slot % kSlotRing] = atomicAdd(work, 1u);
-                            __threadfence_block();
-                            s_pub[slot % kSlotRing] = slot;
-                        } else {
-                            while (s_pub[slot % kSlotRing] != slot) {
-                            }
-                            __threadfence_block();
-                        }
-                        blk = s_block[slot % kSlotRing];
-                    }
-                    blk = __shfl_sync(0xffffffffu, blk, 0);
-                    sub = __shfl_sync(0xffffffffu, sub, 0);
-                    if (blk >= total) {
-                        more = false;
-                        break;
-                    }
-                    q_view = (int)(blk / per_view);
-                    unsigned rem = blk - (unsigned)q_view * per_view;
-                    if (order != nullptr) rem = __ldg(order + rem);
-                    const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
-                    q_x0 = bx * 16 + (int)(sub & 1u) * 8;
-                    q_y0 = by * 16 + (int)(sub >> 1) * 4;
-                    q_next = 0;
-                }
-                const int rank = __popc(idle & lt_mask);
-                const int take = min(32 - q_next, __popc(idle));
-                bool got = false;
-                if (!active && rank < take) {
-                    const int slot = q_next + rank;
-                    px = q_x0 + (slot & 7);
-                    py = q_y0 + (slot >> 3);
-                    pview = q_view;
-                    if (px < W && py < H) {
-                        float o[3], d[3];
-                        camera_ray(cams, pview, px, py, o, d);
-                        if (ray_setup(tr, o, d, r)) {
-                            sh_basis<DEG>(r.d, tr.odd_sign, v.Y);
-                            v.T = 1.f;
-                            v.C[0] = v.C[1] = v.C[2] = 0.f;
-                            trav_begin(tr, r, ts, stk);
-                            got = true;
-                        } else {
-                            float* p = out + (((size_t)pview * H + py) * W + px) * 3;
-                            p[0] = opt.bg[0];
-                            p[1] = opt.bg[1];
-                            p[2] = opt.bg[2];
-                        }
-                    }
-                }
-                active = active || got;
-                q_next += take;
-                idle = __ballot_sync(0xffffffffu, !active);
-            }
-        }
-        if (__ballot_sync(0xffffffffu, active) == 0u) {
-            if (!more) break;
-            continue;
-        }
-        if (active) {
-            if (!trav_step(tr, r, ts, v, stk)) {
-                active = false;
-                float* p = out + (((size_t)pview * H + py) * W + px) * 3;
-                p[0] = fmaf(v.T, opt.bg[0], v.C[0]);
-                p[1] = fmaf(v.T, opt.bg[1], v.C[1]);
-                p[2] = fmaf(v.T, opt.bg[2], v.C[2]);
-            }
         }
     }
     __syncthreads();
@@ -589,12 +539,47 @@ __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* _
 
 static inline unsigned grid1d(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
+// Ask for the smallest shared-memory carveout that still fits the register-limited number of
+// resident CTAs, so the rest of the 256 KB L1/shared array stays L1: the traversal lives off
+// L1 hits on nodes and leaf rows (r01: the driver's default picked a 102 KB carveout for the
+// render kernel's 2 x 17.5 KB).  Returns CTAs per SM.
 template <class K>
-static int persistent_grid(K kernel, int64_t max_ctas) {
+static int tune_carveout(K kernel, int block, size_t dyn_smem) {
+    int dev = 0, per_sm = 0, smem_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (dyn_smem > 0) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, dyn_smem);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && smem_sm > 0 && per_sm > 0) {
+        const size_t need = (size_t)per_sm * (fa.sharedSizeBytes + dyn_smem + 1024);
+        int pct = (int)((need * 100 + smem_sm - 1) / smem_sm);
+        pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
+        cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    }
+    return per_sm;
+}
+
+// tune_carveout once per kernel instance (non-persistent kernels, 256 threads, static smem)
+template <class K>
+static void carveout_once(K kernel) {
+    static std::mutex mu;
+    static std::map<const void*, bool> done;
+    std::lock_guard<std::mutex> lk(mu);
+    const void* key = reinterpret_cast<const void*>(kernel);
+    if (done.count(key)) return;
+    tune_carveout(kernel, 256, 0);
+    done[key] = true;
+}
+
+template <class K>
+static int persistent_grid(K kernel, int64_t max_ctas, size_t dyn_smem = 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    tune_carveout(kernel, 256, dyn_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, dyn_smem);
     int64_t g = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     return (int)(g < max_ctas ? g : (max_ctas > 0 ? max_ctas : 1));
 }
@@ -616,60 +601,44 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kOptDefault;
-        return (v >= 0 && v <= 3) ? v : kOptDefault;
+        return (v >= 0 && v <= 7) ? v : kOptDefault;
     }();
-    static const int refill_min = [] {
-        const char* e = getenv("PO_RENDER_REFILL");
-        const int v = e ? atoi(e) : 0;
-        return (v >= 0 && v <= 32) ? v : 0;
-    }();
-    if (refill_min > 0 && deg == 3 && !f16) {
-        using RFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
-                             int);
-        static const RFn rt[4] = {k_render_refill<3, false, 1>, k_render_refill<3, false, 2>,
-                                  k_render_refill<3, false, 3>, k_render_refill<3, false, 4>};
-        RFn rf = rt[minb - 1];
-        static std::mutex rmu;
-        static std::map<RFn, int> rgrids;
-        int grid;
-        {
-            std::lock_guard<std::mutex> lk(rmu);
-            auto it = rgrids.find(rf);
-            if (it == rgrids.end()) it = rgrids.emplace(rf, persistent_grid(rf, 1 << 30)).first;
-            grid = it->second;
-        }
-        const int g = (int)((int64_t)grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8);
-        rf<<<g, 256, 0, s>>>(tr, cams, n_cams, W, H, opt, out, work, order, refill_min);
-        return cudaGetLastError();
-    }
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
     KFn fn = nullptr;
+    int o = kOptDefault;
     if (deg == 3 && !f16) {
-#define PO_R3(M) {k_render<3, false, M, 0>, k_render<3, false, M, 1>, k_render<3, false, M, 2>, k_render<3, false, M, 3>}
-        static const KFn table[4][4] = {PO_R3(1), PO_R3(2), PO_R3(3), PO_R3(4)};
+#define PO_R3(M)                                                                                                  \
+    {k_render<3, false, M, 0>, k_render<3, false, M, 1>, k_render<3, false, M, 2>, k_render<3, false, M, 3>,     \
+     k_render<3, false, M, 4>, k_render<3, false, M, 5>, k_render<3, false, M, 6>, k_render<3, false, M, 7>}
+        static const KFn table[4][8] = {PO_R3(1), PO_R3(2), PO_R3(3), PO_R3(4)};
 #undef PO_R3
+        o = vopt;
         fn = table[minb - 1][vopt];
     } else {
         PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kOptDefault>);
     }
+    const size_t dyn = (o & kOptSmemRow) ? sizeof(float) * kStageWords * 256 : 0;
     static std::mutex mu;
     static std::map<KFn, int> grids;   // persistent grid size per kernel instance
     int grid;
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = grids.find(fn);
-        if (it == grids.end()) it = grids.emplace(fn, persistent_grid(fn, 1 << 30)).first;
+        if (it == grids.end()) it = grids.emplace(fn, persistent_grid(fn, 1 << 30, dyn)).first;
         grid = it->second;
     }
     const int g = (int)((int64_t)grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8);
-    fn<<<g, 256, 0, s>>>(tr, cams, n_cams, W, H, opt, out, work, order);
+    fn<<<g, 256, dyn, s>>>(tr, cams, n_cams, W, H, opt, out, work, order);
     return cudaGetLastError();
 }
 
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
                                const RenderOpts& opt, float* out, double* aux, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    PO_DISPATCH(deg, f16, k_render_rays<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out, aux));
+    PO_DISPATCH(deg, f16, {
+        carveout_once(k_render_rays<DEG, F16>);
+        k_render_rays<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out, aux);
+    });
     return cudaGetLastError();
 }
 
@@ -677,14 +646,17 @@ cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* r
                             const double* aux, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
                             cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    PO_DISPATCH(deg, f16,
-                k_backward<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, opt, grad_sigma, grad_sh));
+    PO_DISPATCH(deg, f16, {
+        carveout_once(k_backward<DEG, F16>);
+        k_backward<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, opt, grad_sigma, grad_sh);
+    });
     return cudaGetLastError();
 }
 
 cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
                          int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    carveout_once(k_trace);
     k_trace<<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, max_leaves, leaf_ids, counts, node_counts);
     return cudaGetLastError();
 }
@@ -692,6 +664,7 @@ cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float 
 cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, int W, int H, float gamma,
                          unsigned long long* counters, cudaStream_t s) {
     dim3 grid((W + 15) / 16, (H + 15) / 16, n_cams);
+    carveout_once(k_stats);
     k_stats<<<grid, 256, 0, s>>>(tr, cams, W, H, gamma, counters);
     return cudaGetLastError();
 }

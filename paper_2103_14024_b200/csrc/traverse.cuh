@@ -101,6 +101,7 @@ struct SmemStack {
 //   kOptParentCache  register copy of the current level-(D-1) node's 8 child entries
 //   kOptLeafStep     fast neighbour step when the box is a single leaf-level cell
 constexpr int kOptParentCache = 1, kOptLeafStep = 2;
+constexpr int kOptSmemRow = 4;   // (render visitor) leaf rows staged in shared memory by cp.async
 constexpr int kOptDefault = 0;
 
 template <int OPT = kOptDefault, class V>

@@ -367,3 +367,22 @@ def test_optimizer_step_matches_oracle(env):
     s1, k1 = tree.read_leaves()
     _grad_ok((t.sigma.astype(np.float64) - s1) / lr, gs, "sgd sigma")
     _grad_ok((t.sh.astype(np.float64) - k1) / lr, gk, "sgd sh")
+
+
+def test_optimizer_descends_on_fixed_batch(env, c0_tree):
+    """Repeated SGD steps on one batch: the Eq. (3) loss decreases every step and
+    the tree moves toward the unperturbed one that rendered the targets."""
+    po, om, torch = env
+    from paper_2103_14024_b200.optim import OctreeOptimizer
+    cams = np.concatenate([gen.orbit_camera(3.0, 30.0 * i, 20.0, 64, 64, 70.0) for i in range(6)])
+    gt = po.tree_from_gen(c0_tree)
+    rays = po.po_camera_rays(po.cams_tensor(cams), 64, 64).reshape(-1, 6)
+    target = po.po_render_rays(gt, rays, gamma=0.0)
+    g = rng(80)
+    sig = (c0_tree.sigma + g.normal(0.0, 0.5, c0_tree.sigma.shape)).astype(np.float32)
+    sh = (c0_tree.sh + g.normal(0.0, 0.3, c0_tree.sh.shape)).astype(np.float32)
+    tree = po.po_tree_create(c0_tree.child, sig, sh, c0_tree.depth, 1, c0_tree.bbox_min, c0_tree.edge)
+    opt = OctreeOptimizer(tree, lr=1.0, gamma=0.0)   # oracle sweep: 5.03 -> 3.22 over 8 steps at lr 1
+    losses = [opt.step(rays, target).item() for _ in range(8)]
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses
+    assert losses[-1] < 0.8 * losses[0], losses
