@@ -158,7 +158,8 @@ def run_ours(args):
     # algorithmic bytes per launch: counters of the same traversal
     B = t_gen.basis_dim
     row_bytes = 3 * B * (2 if payload == po.PO_F16 else 4)
-    stats = {"leaf_visits": 0, "sh_rows": 0, "nodes": 0, "hit_rays": 0}
+    stats = {"leaf_visits": 0, "sh_rows": 0, "nodes": 0, "hit_rays": 0, "boxes": 0, "leaf_level_boxes": 0,
+             "warp_boxes": 0}
     for s in range(args.warmup, args.warmup + args.steps):
         v = view_of(s)
         st = po.po_render_stats(tree, cams[v:v + 1], W, H, gamma=GAMMA)
@@ -240,6 +241,10 @@ def run_ours(args):
                       | ({"l2": f"NOT flushed ({args.l2}): analysis only"} if args.l2 != "flush" else {}),
             "mrays_per_s": round(fps * W * H / 1e6, 1),
             "leaf_visits_per_frame": stats["leaf_visits"] / K,
+            "traversal_per_frame": {"boxes": stats["boxes"] / K, "leaf_level_boxes": stats["leaf_level_boxes"] / K,
+                                    "internal_nodes_met": stats["nodes"] / K, "hit_rays": stats["hit_rays"] / K,
+                                    "simt_step_efficiency": round(stats["boxes"] / max(1, 32 * stats["warp_boxes"]),
+                                                                  4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": f"po::k_render<3,{int(payload == po.PO_F16)}>", "peak_source": peak_src,

@@ -162,8 +162,9 @@ po_status po_trace(const po_tree* tree, const float* rays, int64_t n, const po_r
                    int32_t max_leaves, int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, po_stream stream);
 
 /* po_render_stats: counters of the po_render traversal over n_cams views, ADDED to
- * device uint64 counters[4] = {leaf visits, leaf visits with sigma~ > 0 (SH row read),
- * internal nodes met (root included), rays that hit the bbox}. */
+ * device uint64 counters[7] = {leaf visits, leaf visits with sigma~ > 0 (SH row read),
+ * internal nodes met (root included), rays that hit the bbox, boxes stepped through (leaf or
+ * empty), of which leaf-level cells, sum over 8x4-pixel warps of the longest ray's boxes}. */
 po_status po_render_stats(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                           const po_render_opts* opts, unsigned long long* counters, po_stream stream);
 

@@ -34,7 +34,8 @@ def build(force: bool = False) -> str:
 
 class OrTree(ctypes.Structure):
     _fields_ = [("child", ctypes.c_void_p), ("n_nodes", ctypes.c_int64), ("sigma", ctypes.c_void_p),
-                ("sh", ctypes.c_void_p), ("n_leaves", ctypes.c_int64), ("depth", ctypes.c_int32),
+                ("sh", ctypes.c_void_p), ("sh32", ctypes.c_void_p), ("n_leaves", ctypes.c_int64),
+                ("depth", ctypes.c_int32),
                 ("sh_degree", ctypes.c_int32), ("sh_cs", ctypes.c_int32), ("pad_", ctypes.c_int32),
                 ("bbox_min", ctypes.c_double * 3), ("edge", ctypes.c_double)]
 
@@ -51,7 +52,7 @@ def lib():
         _lib.or_trace_ray.argtypes = [P, P, ctypes.c_int, I64, P, P, P, P]
         _lib.or_trace_ray.restype = I64
         _lib.or_render.argtypes = [P, P, I64, D, P, ctypes.c_int, P, P, P, I32, P, P, ctypes.c_int]
-        _lib.or_backward.argtypes = [P, P, I64, D, P, P, P, P, ctypes.c_int]
+        _lib.or_backward.argtypes = [P, P, I64, D, P, P, P, P, ctypes.c_int, P, P]
         _lib.or_tie_flags.argtypes = [P, P, I64, D, D, D, P, ctypes.c_int]
     return _lib
 
@@ -65,12 +66,19 @@ class OracleTree:
 
     def __init__(self, tree, sh_cs: int = 1, sigma=None, sh=None):
         self.child = np.ascontiguousarray(tree.child, dtype=np.uint32)
-        # widened exactly to float64 (fp32 / fp16 values are representable)
+        # sigma widened exactly to float64; SH kept as given: float64 arrays (finite-difference
+        # tests) are used directly, fp32 / fp16 ones are stored as fp32 and widened exactly in C
         self.sigma = np.ascontiguousarray(tree.sigma if sigma is None else sigma, dtype=np.float64)
-        self.sh = np.ascontiguousarray(tree.sh if sh is None else sh, dtype=np.float64)
+        arr = tree.sh if sh is None else sh
+        if np.asarray(arr).dtype == np.float64:
+            self.sh, self.sh32 = np.ascontiguousarray(arr), None
+        else:
+            self.sh, self.sh32 = None, np.ascontiguousarray(arr, dtype=np.float32)
         self.B = (tree.sh_degree + 1) ** 2
         self.n_leaves = self.sigma.shape[0]
-        self.desc = OrTree(_ptr(self.child).value, self.child.shape[0], _ptr(self.sigma).value, _ptr(self.sh).value,
+        self.desc = OrTree(_ptr(self.child).value, self.child.shape[0], _ptr(self.sigma).value,
+                           _ptr(self.sh).value if self.sh is not None else None,
+                           _ptr(self.sh32).value if self.sh32 is not None else None,
                            self.n_leaves, tree.depth, tree.sh_degree, sh_cs, 0,
                            (ctypes.c_double * 3)(*[float(v) for v in tree.bbox_min]), float(tree.edge))
 
@@ -127,15 +135,20 @@ def render(ot: OracleTree, rays, gamma: float = 0.01, bg=(1.0, 1.0, 1.0), mode: 
     return dict(rgb=rgb, T=T, n_proc=n_proc, nodes_met=nodes, leaf_ids=ids)
 
 
-def backward(ot: OracleTree, rays, dL_dC, gamma: float = 0.0, bg=(1.0, 1.0, 1.0), nthreads: int = 0):
-    """Returns (grad_sigma [n_leaves], grad_sh [n_leaves, B, 3]) in float64."""
+def backward(ot: OracleTree, rays, dL_dC, gamma: float = 0.0, bg=(1.0, 1.0, 1.0), nthreads: int = 0,
+             with_scale: bool = False):
+    """Returns (grad_sigma [n_leaves], grad_sh [n_leaves, B, 3]) in float64; with_scale also
+    returns the per-component magnitude of the summed terms (rounding-error yardstick)."""
     rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
     g = np.ascontiguousarray(dL_dC, dtype=np.float64).reshape(-1, 3)
     bg = np.ascontiguousarray(bg, dtype=np.float64)
     gs = np.zeros(ot.n_leaves)
     gk = np.zeros((ot.n_leaves, ot.B, 3))
-    lib().or_backward(ot.ref, _ptr(rays), rays.shape[0], gamma, _ptr(bg), _ptr(g), _ptr(gs), _ptr(gk), nthreads)
-    return gs, gk
+    ss = np.zeros(ot.n_leaves) if with_scale else None
+    sk = np.zeros((ot.n_leaves, ot.B, 3)) if with_scale else None
+    lib().or_backward(ot.ref, _ptr(rays), rays.shape[0], gamma, _ptr(bg), _ptr(g), _ptr(gs), _ptr(gk), nthreads,
+                      _ptr(ss), _ptr(sk))
+    return (gs, gk, ss, sk) if with_scale else (gs, gk)
 
 
 def tie_flags(ot: OracleTree, rays, gamma: float = 0.01, tol_plane: float = 1e-6, tol_gamma: float = 2e-2,

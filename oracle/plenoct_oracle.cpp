@@ -39,7 +39,8 @@ typedef struct {
     const uint32_t* child;   // [n_nodes][8], tag<<30 | index (reading Q1)
     int64_t n_nodes;
     const double* sigma;     // [n_leaves] sigma-tilde (the caller widens fp32/fp16 exactly)
-    const double* sh;        // [n_leaves][B][3]
+    const double* sh;        // [n_leaves][B][3], or NULL when sh32 is given
+    const float* sh32;       // [n_leaves][B][3] fp32 values (widened exactly when read), used if sh == NULL
     int64_t n_leaves;
     int32_t depth;           // D
     int32_t sh_degree;       // l_max
@@ -254,10 +255,13 @@ inline double sigmoid(double z) { return 1.0 / (1.0 + std::exp(-z)); }
 
 // Eq. (5): c_ch = S(sum_b k_{b,ch} Y_b)
 inline void leaf_color(const or_tree* T, int64_t leaf, const double* Y, int B, double c[3]) {
-    const double* k = T->sh + leaf * (int64_t)B * 3;
+    const int64_t off = leaf * (int64_t)B * 3;
     for (int ch = 0; ch < 3; ++ch) {
         double z = 0.0;
-        for (int b = 0; b < B; ++b) z += k[b * 3 + ch] * Y[b];
+        for (int b = 0; b < B; ++b) {
+            const double k = T->sh ? T->sh[off + b * 3 + ch] : (double)T->sh32[off + b * 3 + ch];
+            z += k * Y[b];
+        }
         c[ch] = sigmoid(z);
     }
 }
@@ -420,9 +424,12 @@ int or_render(const or_tree* T, const double* rays, int64_t n, double gamma, con
 }
 
 // Analytic backward with direct suffix sums in double.
-// grad_sigma [n_leaves], grad_sh [n_leaves][B][3] are ACCUMULATED (+=).
+// grad_sigma [n_leaves], grad_sh [n_leaves][B][3] are ACCUMULATED (+=).  If non-NULL,
+// sigma_scale / sh_scale accumulate the magnitude of what was summed into each component
+// (|delta| sum_ch |g| (|c T| + |S|) and |g w c (1-c) Y|): the natural yardstick for the rounding
+// error of any implementation that forms and sums those terms in finite precision.
 int or_backward(const or_tree* T, const double* rays, int64_t n, double gamma, const double* bg, const double* dL_dC,
-                double* grad_sigma, double* grad_sh, int nthreads) {
+                double* grad_sigma, double* grad_sh, int nthreads, double* sigma_scale, double* sh_scale) {
     int B = (T->sh_degree + 1) * (T->sh_degree + 1);
     int nt = set_threads(nthreads);
 #pragma omp parallel num_threads(nt)
@@ -469,12 +476,19 @@ int or_backward(const or_tree* T, const double* rays, int64_t n, double gamma, c
                 double st = (double)T->sigma[leaf];
                 double delta = cx.segs[k].t1 - cx.segs[k].t0;
                 if (st > 0.0) {   // ReLU gate: zero for sigma~ <= 0 (reading Q21)
-                    double gs = 0.0;
-                    for (int ch = 0; ch < 3; ++ch)
+                    double gs = 0.0, mag = 0.0;
+                    for (int ch = 0; ch < 3; ++ch) {
                         gs += g[ch] * (col[(size_t)k * 3 + ch] * Ti[k + 1] - S[(size_t)k * 3 + ch]);
+                        mag += std::fabs(g[ch]) * (std::fabs(col[(size_t)k * 3 + ch] * Ti[k + 1]) +
+                                                   std::fabs(S[(size_t)k * 3 + ch]));
+                    }
                     gs *= delta;
 #pragma omp atomic
                     grad_sigma[leaf] += gs;
+                    if (sigma_scale) {
+#pragma omp atomic
+                        sigma_scale[leaf] += std::fabs(delta) * mag;
+                    }
                 }
                 for (int ch = 0; ch < 3; ++ch) {
                     double c = col[(size_t)k * 3 + ch];
@@ -483,6 +497,10 @@ int or_backward(const or_tree* T, const double* rays, int64_t n, double gamma, c
                     for (int b = 0; b < B; ++b) {
 #pragma omp atomic
                         grad_sh[(leaf * B + b) * 3 + ch] += gz * Y[b];
+                        if (sh_scale) {
+#pragma omp atomic
+                            sh_scale[(leaf * B + b) * 3 + ch] += std::fabs(gz * Y[b]);
+                        }
                     }
                 }
             }

@@ -289,15 +289,16 @@ def po_trace(tree: PlenOctree, rays, max_leaves: int = 64, gamma: float = 0.01, 
 
 
 def po_render_stats(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.01, stream=None):
-    """Returns dict(leaf_visits, sh_rows, nodes, hit_rays) for one po_render over ``cams``."""
+    """Traversal counters for one po_render over ``cams`` (see po_render_stats in plenoct.h)."""
     import torch
     cams = _need(cams, torch.float32, (16,))
-    ctr = torch.zeros(4, dtype=torch.int64, device=cams.device)
+    ctr = torch.zeros(7, dtype=torch.int64, device=cams.device)
     o = _opts(gamma, (1.0, 1.0, 1.0))
     _check(lib().po_render_stats(tree.handle, _ptr(cams), cams.shape[0], W, H, ctypes.byref(o), _ptr(ctr),
                                  _stream(stream)))
     v = ctr.cpu().tolist()
-    return dict(leaf_visits=v[0], sh_rows=v[1], nodes=v[2], hit_rays=v[3])
+    return dict(leaf_visits=v[0], sh_rows=v[1], nodes=v[2], hit_rays=v[3], boxes=v[4], leaf_level_boxes=v[5],
+                warp_boxes=v[6])
 
 
 def launch_count() -> int:

@@ -30,6 +30,9 @@ struct po_tree {
     int cam_cap = 0;
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
+    // empty-space skipping grid (DevTree::macro): level M = min(5, D - 1)
+    uint8_t* d_macro = nullptr;
+    int macro_level = 0;
     // centre-out order of the 16x16 pixel blocks of a W x H view (built once per size)
     unsigned* d_order = nullptr;
     int order_w = 0, order_h = 0;
@@ -122,7 +125,67 @@ po::DevTree dev_tree(const po_tree* t) {
     for (int k = 0; k < 3; ++k) d.bmin[k] = t->desc.bbox_min[k];
     d.scale = (float)std::ldexp(1.0, t->desc.max_depth) / t->desc.bbox_edge;
     d.odd_sign = t->desc.sh_sign == PO_SH_NO_CS ? -1.f : 1.f;
+    d.macro = t->d_macro;
+    d.macro_shift = t->desc.max_depth - t->macro_level;
+    d.macro_n = 1 << t->macro_level;
     return d;
+}
+
+// Level-M occupancy of the leaves and its Chebyshev distance transform (multi-source BFS over
+// the 26-neighbourhood), capped at 255.  Host side, once per tree (a0).
+std::vector<uint8_t> build_macro_grid(const uint32_t* child, int D, int M) {
+    const int n = 1 << M;
+    std::vector<uint8_t> occ((size_t)n * n * n, 0);
+    struct Item { uint32_t node; int level; int x, y, z; };
+    std::vector<Item> st{{0u, 0, 0, 0, 0}};
+    while (!st.empty()) {
+        const Item it = st.back();
+        st.pop_back();
+        for (int o = 0; o < 8; ++o) {
+            const uint32_t e = child[(size_t)it.node * 8 + o];
+            const uint32_t tag = e >> 30;
+            if (tag == po::kTagEmpty) continue;
+            const int L = it.level + 1;
+            const int x = it.x * 2 + ((o >> 2) & 1), y = it.y * 2 + ((o >> 1) & 1), z = it.z * 2 + (o & 1);
+            if (tag == po::kTagInternal) {
+                st.push_back({e & po::kIdxMask, L, x, y, z});
+            } else if (L >= M) {
+                const int s = L - M;
+                occ[((size_t)(x >> s) * n + (y >> s)) * n + (z >> s)] = 1;
+            } else {
+                const int s = M - L;
+                for (int a = x << s; a < (x + 1) << s; ++a)
+                    for (int b = y << s; b < (y + 1) << s; ++b)
+                        for (int c = z << s; c < (z + 1) << s; ++c) occ[((size_t)a * n + b) * n + c] = 1;
+            }
+        }
+    }
+    std::vector<uint8_t> dist((size_t)n * n * n, 255);
+    std::vector<int> frontier, next;
+    for (size_t i = 0; i < occ.size(); ++i)
+        if (occ[i]) {
+            dist[i] = 0;
+            frontier.push_back((int)i);
+        }
+    for (int d = 1; d < 255 && !frontier.empty(); ++d) {
+        next.clear();
+        for (int i : frontier) {
+            const int a = i / (n * n), b = (i / n) % n, c = i % n;
+            for (int da = -1; da <= 1; ++da)
+                for (int db = -1; db <= 1; ++db)
+                    for (int dc = -1; dc <= 1; ++dc) {
+                        const int aa = a + da, bb = b + db, cc = c + dc;
+                        if (aa < 0 || bb < 0 || cc < 0 || aa >= n || bb >= n || cc >= n) continue;
+                        const size_t j = ((size_t)aa * n + bb) * n + cc;
+                        if (dist[j] == 255) {
+                            dist[j] = (uint8_t)d;
+                            next.push_back((int)j);
+                        }
+                    }
+        }
+        frontier.swap(next);
+    }
+    return dist;
 }
 
 po_status check_opts(const po_render_opts* o, po::RenderOpts* out) {
@@ -247,6 +310,14 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sigma)"));
     e = cudaMalloc(&t->d_sh, (size_t)std::max<int64_t>(n_leaves, 1) * row * elt);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
+    {
+        t->macro_level = std::min(5, D - 1);
+        const std::vector<uint8_t> grid = build_macro_grid(child, D, t->macro_level);
+        e = cudaMalloc(&t->d_macro, grid.size());
+        if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(macro)"));
+        e = cudaMemcpy(t->d_macro, grid.data(), grid.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cleanup(cuda_status(e, "upload macro"));
+    }
     e = cudaMalloc(&t->d_work, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
     e = cudaMemset(t->d_work, 0, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
@@ -291,6 +362,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_work) cudaFree(t->d_work);
     if (t->d_img) cudaFree(t->d_img);
     if (t->d_order) cudaFree(t->d_order);
+    if (t->d_macro) cudaFree(t->d_macro);
     t->d_child = nullptr;
     delete t;
     return PO_OK;

@@ -211,8 +211,12 @@ struct TraceVisitor {
 struct StatsVisitor {
     const DevTree& tr;
     float T, gamma;
-    unsigned long long leaves, sh_rows, nodes;
+    unsigned long long leaves, sh_rows, nodes, boxes, leaf_level_boxes;
     __device__ __forceinline__ void on_node() { ++nodes; }
+    __device__ __forceinline__ void on_box(int shift) {
+        ++boxes;
+        leaf_level_boxes += (shift == 0);
+    }
     __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
         ++leaves;
         const float st = __ldg(tr.sigma + idx);
@@ -456,26 +460,32 @@ __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restri
     if (node_counts) node_counts[i] = v.nodes;
 }
 
+constexpr int kStatCounters = 7;
 __global__ void __launch_bounds__(256) k_stats(DevTree tr, const po_camera* __restrict__ cams, int W, int H,
                                                float gamma, unsigned long long* __restrict__ counters) {
     PO_DECLARE_STACK(stk);
     int px, py;
-    unsigned long long v4[4] = {0, 0, 0, 0};
+    unsigned long long v4[kStatCounters] = {0, 0, 0, 0, 0, 0, 0};
     if (tile_pixel(W, H, px, py)) {
         float o[3], d[3];
         camera_ray(cams, blockIdx.z, px, py, o, d);
         RayState r;
         if (ray_setup(tr, o, d, r)) {
-            StatsVisitor v{tr, 1.f, gamma, 0, 0, 0};
+            StatsVisitor v{tr, 1.f, gamma, 0, 0, 0, 0, 0};
             traverse(tr, r, v, stk);
             v4[0] = v.leaves;
             v4[1] = v.sh_rows;
             v4[2] = v.nodes;
             v4[3] = 1;
+            v4[4] = v.boxes;
+            v4[5] = v.leaf_level_boxes;
         }
     }
+    // SIMT cost: boxes of the longest ray of each warp (the warp executes that many steps)
+    v4[6] = (threadIdx.x & 31) == 0 ? __reduce_max_sync(0xffffffffu, (unsigned)v4[4])
+                                    : (__reduce_max_sync(0xffffffffu, (unsigned)v4[4]), 0u);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kStatCounters; ++k) {
         unsigned long long s = v4[k];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -600,22 +610,30 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     }();
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
-        const int v = e ? atoi(e) : kOptDefault;
-        return (v >= 0 && v <= 7) ? v : kOptDefault;
+        const int v = e ? atoi(e) : kRenderOptDefault;
+        return (v >= 0 && v <= 15) ? v : kRenderOptDefault;
     }();
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
     KFn fn = nullptr;
-    int o = kOptDefault;
-    if (deg == 3 && !f16) {
-#define PO_R3(M)                                                                                                  \
-    {k_render<3, false, M, 0>, k_render<3, false, M, 1>, k_render<3, false, M, 2>, k_render<3, false, M, 3>,     \
-     k_render<3, false, M, 4>, k_render<3, false, M, 5>, k_render<3, false, M, 6>, k_render<3, false, M, 7>}
-        static const KFn table[4][8] = {PO_R3(1), PO_R3(2), PO_R3(3), PO_R3(4)};
+    int o = kRenderOptDefault;
+    if (deg == 3 && !f16 && (minb != 2 || vopt != kRenderOptDefault)) {
+        // A/B instances: every variant at 2 CTAs/SM, the default variant at 1/3/4 CTAs/SM
+#define PO_R3(O0, O1, O2, O3) k_render<3, false, 2, O0>, k_render<3, false, 2, O1>, k_render<3, false, 2, O2>, \
+                              k_render<3, false, 2, O3>
+        static const KFn by_opt[16] = {PO_R3(0, 1, 2, 3), PO_R3(4, 5, 6, 7), PO_R3(8, 9, 10, 11),
+                                       PO_R3(12, 13, 14, 15)};
 #undef PO_R3
-        o = vopt;
-        fn = table[minb - 1][vopt];
+        static const KFn by_minb[4] = {k_render<3, false, 1, kRenderOptDefault>, nullptr,
+                                       k_render<3, false, 3, kRenderOptDefault>,
+                                       k_render<3, false, 4, kRenderOptDefault>};
+        if (minb == 2) {
+            o = vopt;
+            fn = by_opt[vopt];
+        } else {
+            fn = by_minb[minb - 1];
+        }
     } else {
-        PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kOptDefault>);
+        PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kRenderOptDefault>);
     }
     const size_t dyn = (o & kOptSmemRow) ? sizeof(float) * kStageWords * 256 : 0;
     static std::mutex mu;

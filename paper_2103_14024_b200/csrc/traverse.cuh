@@ -19,6 +19,9 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <type_traits>
+#include <utility>
+
 namespace po {
 
 constexpr uint32_t kTagEmpty = 0u, kTagInternal = 1u, kTagLeaf = 2u;
@@ -34,6 +37,11 @@ struct DevTree {
     float bmin[3];
     float scale;                          // 2^D / edge
     float odd_sign;                       // +1 (Condon-Shortley reading) or -1
+    // empty-space skipping: Chebyshev distance (in level-M cells, capped at 255) from each
+    // level-M cell to the nearest level-M cell that contains a leaf; [n][n][n], n = 2^M
+    const uint8_t* __restrict__ macro;
+    int32_t macro_shift;                  // D - M
+    int32_t macro_n;                      // 2^M
 };
 
 struct RayState {
@@ -102,7 +110,22 @@ struct SmemStack {
 //   kOptLeafStep     fast neighbour step when the box is a single leaf-level cell
 constexpr int kOptParentCache = 1, kOptLeafStep = 2;
 constexpr int kOptSmemRow = 4;   // (render visitor) leaf rows staged in shared memory by cp.async
+// kOptMacroSkip: when the ray enters a level-M cell whose distance d to the nearest occupied
+// level-M cell is >= 1, jump in one step to the exit of the (2d-1)^3 block of level-M cells
+// around it (all empty by definition of d) instead of stepping through the empty octree
+// boxes one by one.  Leaves are never skipped, so the visited sequence is unchanged.
+constexpr int kOptMacroSkip = 8;
+// variant of the po_render kernel (po_render_stats / po_trace keep kOptDefault so their
+// internal-node counts stay the oracle's algorithm-independent "nodes met")
+constexpr int kRenderOptDefault = 0;
 constexpr int kOptDefault = 0;
+
+// Optional visitor hook on_box(shift), called once per box the ray steps through (leaf or
+// empty; shift = log2 of the box edge in leaf cells).  Only the statistics visitor has it.
+template <class V, class = void>
+struct HasOnBox : std::false_type {};
+template <class V>
+struct HasOnBox<V, std::void_t<decltype(std::declval<V&>().on_box(0))>> : std::true_type {};
 
 template <int OPT = kOptDefault, class V>
 __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V& vis, const SmemStack& stk) {
@@ -121,7 +144,51 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     uint32_t pnode = 0xFFFFFFFFu;
     uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
     const uint4* __restrict__ child4 = reinterpret_cast<const uint4*>(tr.child);
+    bool check_macro = (OPT & kOptMacroSkip) != 0 && tr.macro != nullptr;
     while (true) {
+        if constexpr ((OPT & kOptMacroSkip) != 0) {
+            if (check_macro) {
+                const int ms = tr.macro_shift, mn = tr.macro_n;
+                const int m0 = c[0] >> ms, m1 = c[1] >> ms, m2 = c[2] >> ms;
+                const int dist = __ldg(tr.macro + ((m0 * mn + m1) * mn + m2));
+                if (dist > 0) {
+                    const int rr = dist - 1;
+                    const int mm[3] = {m0, m1, m2};
+                    int lo[3], hi[3];
+                    float te[3];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        lo[k] = max(mm[k] - rr, 0) << ms;
+                        hi[k] = min(mm[k] + rr + 1, mn) << ms;
+                        te[k] = ((float)((r.dg[k] >= 0.f) ? hi[k] : lo[k]) - r.o[k]) * r.inv[k];
+                    }
+                    const float texit = fminf(fminf(te[0], te[1]), te[2]);
+                    const int ax = (te[0] == texit) ? 0 : ((te[1] == texit) ? 1 : 2);
+                    if (!(texit < r.tfar)) return;
+                    t = texit;
+                    int nc[3];
+                    bool out = false;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const float p = fmaf(t, r.dg[k], r.o[k]);
+                        const float f = floorf(p);
+                        const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
+                        const int nex = (r.dg[k] > 0.f) ? hi[k] : lo[k] - 1;
+                        nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), hi[k] - 1);
+                        out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
+                    }
+                    if (out) return;
+                    const int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
+                    // the stack is only valid down to the current restart level L
+                    L = min(L, D - 1 - (31 - __clz(diff)));
+                    c[0] = nc[0];
+                    c[1] = nc[1];
+                    c[2] = nc[2];
+                    continue;
+                }
+                check_macro = false;   // occupied level-M cell: plain traversal until we leave it
+            }
+        }
         uint32_t node = stk[L];
         uint32_t e;
         int shift;
@@ -149,6 +216,7 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         // the box of entry e: level L+1, 2^shift leaf cells per axis.  Exit t per axis,
         // branch-free: an axis with dg == 0 uses its upper face and inv = +inf, giving +inf
         // (or NaN when the origin sits exactly on that face), which fminf ignores.
+        if constexpr (HasOnBox<V>::value) vis.on_box(shift);
         const int size = 1 << shift;
         int lo[3];
         float te[3];
@@ -194,82 +262,9 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         c[0] = nc[0];
         c[1] = nc[1];
         c[2] = nc[2];
+        if constexpr ((OPT & kOptMacroSkip) != 0)
+            check_macro = tr.macro != nullptr && (diff >> tr.macro_shift) != 0;   // entered a new level-M cell
     }
-}
-
-// Resumable form of the same traversal (identical arithmetic, one box per call), for kernels
-// that refill finished lanes with new rays between steps.
-struct TravState {
-    float t;
-    int c[3];
-    int L;
-};
-
-__device__ __forceinline__ void trav_begin(const DevTree& tr, const RayState& r, TravState& s, const SmemStack& stk) {
-    const int G = 1 << tr.depth;
-    s.t = r.tnear;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) s.c[k] = min(max(cell_of(r.o[k], r.dg[k], s.t), 0), G - 1);
-    stk[0] = 0u;
-    s.L = 0;
-}
-
-// One box: descend to the entry containing the current cell, visit it if it is a leaf,
-// advance to the next cell.  Returns false once the ray is finished.
-template <class V>
-__device__ __forceinline__ bool trav_step(const DevTree& tr, const RayState& r, TravState& s, V& vis,
-                                          const SmemStack& stk) {
-    const int D = tr.depth;
-    const int G = 1 << D;
-    int L = s.L;
-    uint32_t node = stk[L];
-    uint32_t e;
-    int shift;
-    while (true) {
-        shift = D - 1 - L;
-        const int oct = (((s.c[0] >> shift) & 1) << 2) | (((s.c[1] >> shift) & 1) << 1) | ((s.c[2] >> shift) & 1);
-        e = __ldg(tr.child + (node * 8u + (uint32_t)oct));
-        if ((e >> 30) != kTagInternal) break;
-        node = e & kIdxMask;
-        ++L;
-        stk[L] = node;
-        vis.on_node();
-    }
-    const int size = 1 << shift;
-    int lo[3];
-    float te[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        lo[k] = s.c[k] & ~(size - 1);
-        const int face = (r.dg[k] >= 0.f) ? lo[k] + size : lo[k];
-        te[k] = ((float)face - r.o[k]) * r.inv[k];
-    }
-    const float texit = fminf(fminf(te[0], te[1]), te[2]);
-    const int ax = (te[0] == texit) ? 0 : ((te[1] == texit) ? 1 : 2);
-    const float tout = fminf(texit, r.tfar);
-    if ((e >> 30) == kTagLeaf && tout > s.t) {
-        if (!vis.on_leaf(e & kIdxMask, s.t, tout)) return false;
-    }
-    if (!(texit < r.tfar)) return false;
-    s.t = texit;
-    int nc[3];
-    bool out = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const float p = fmaf(s.t, r.dg[k], r.o[k]);
-        const float f = floorf(p);
-        const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
-        const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;
-        nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
-        out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
-    }
-    if (out) return false;
-    const int diff = (s.c[0] ^ nc[0]) | (s.c[1] ^ nc[1]) | (s.c[2] ^ nc[2]);
-    s.L = D - 1 - (31 - __clz(diff));
-    s.c[0] = nc[0];
-    s.c[1] = nc[1];
-    s.c[2] = nc[2];
-    return true;
 }
 
 // ---------------------------------------------------------------------------------

@@ -1,0 +1,90 @@
+"""Parity at BASELINE.json's full sizes, in the launch configurations bench.py times, on
+outputs the oracle computes one by one (sampled pixels / a ray subset)."""
+import numpy as np
+import pytest
+
+import gen
+from conftest import rng
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(oracle_mod):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+    import paper_2103_14024_b200 as po
+    return po, oracle_mod, torch
+
+
+@pytest.fixture(scope="module")
+def c3_tree():
+    return gen.scene_c3()
+
+
+def _tie_free(om, ot, rays, gamma):
+    return om.tie_flags(ot, rays, gamma=gamma if gamma > 0 else 1e-30) == 0
+
+
+def test_c3_fp16_full_frame_sampled(env, c3_tree):
+    """c3: 1920x1080, depth 10, fp16 payload, the bench launch; 2048 sampled pixels."""
+    po, om, torch = env
+    tree = po.tree_from_gen(c3_tree, payload=po.PO_F16)
+    cam, W, H = gen.config_camera("c3")
+    img = po.po_render(tree, po.cams_tensor(cam), W, H, gamma=0.01).reshape(-1, 3).cpu().numpy()
+    rays = om.camera_rays(cam, W, H)
+    pick = rng(90).choice(W * H, 2048, replace=False)
+    deq = c3_tree.sh.astype(np.float16).astype(np.float32)          # reading Q20 / Q29 check 1
+    ot_q = om.OracleTree(c3_tree, sh=deq)
+    ref_q = om.render(ot_q, rays[pick], gamma=0.01)
+    ok = _tie_free(om, ot_q, rays[pick], 0.01)
+    assert ok.sum() > 1000
+    assert np.abs(img[pick][ok] - ref_q["rgb"][ok]).max() <= 1e-4
+    del ot_q, deq
+    ot = om.OracleTree(c3_tree)                                      # Q29 check 2: fp32 values
+    ref = om.render(ot, rays[pick], gamma=0.01)
+    ok2 = ok & _tie_free(om, ot, rays[pick], 0.01)
+    assert np.abs(img[pick][ok2] - ref["rgb"][ok2]).max() <= 2e-3
+    assert (ref["n_proc"] > 0).sum() > 300      # the sample really hits the scene (458 of 2048 in r01)
+
+
+def test_c1_backward_ray_subset(env, c1_tree):
+    """c1 tree (3.4 M leaves), gamma = 0, 4096 training rays: GPU gradients vs the oracle."""
+    po, om, torch = env
+    cams = gen.fibonacci_hemisphere(100, 4.0, 800, 800, 1111.111)
+    g = rng(91)
+    pick = g.choice(100 * 800 * 800, 4096, replace=False)
+    rays = gen.camera_rays_f32(cams, 800, 800, pick // 640000, pick % 640000)
+    ot = om.OracleTree(c1_tree)
+    r64 = rays.astype(np.float64)
+    ok = _tie_free(om, ot, r64, 1e-30)
+    rays, r64 = rays[ok], r64[ok]
+    dL = g.normal(size=(rays.shape[0], 3)).astype(np.float32)
+    tree = po.tree_from_gen(c1_tree)
+    gs = torch.zeros(tree.n_leaves, device="cuda")
+    gk = torch.zeros((tree.n_leaves, 16, 3), device="cuda")
+    rt = torch.from_numpy(rays).cuda()
+    aux = torch.empty((rays.shape[0], 4), dtype=torch.float64, device="cuda")
+    po.po_render_rays(tree, rt, aux=aux, gamma=0.0)
+    po.po_render_backward(tree, rt, torch.from_numpy(dL).cuda(), gs, gk, aux=aux, gamma=0.0)
+    rs, rk, ss, sk = om.backward(ot, r64, dL.astype(np.float64), gamma=0.0, with_scale=True)
+    gs, gk = gs.cpu().numpy().astype(np.float64), gk.cpu().numpy().astype(np.float64)
+    touched = np.flatnonzero((rs != 0) | (np.abs(rk).sum((1, 2)) != 0))
+    assert touched.size > 1000
+    for a, b, sc, tag in ((gs[touched], rs[touched], ss[touched], "sigma"),
+                          (gk[touched], rk[touched], sk[touched], "sh")):
+        a, b, sc = a.ravel(), b.ravel(), sc.ravel()
+        rel = np.linalg.norm(a - b) / np.linalg.norm(b)
+        assert rel <= 1e-3, (tag, rel)
+        # per component (reading Q26 at c1 scale): relative to the magnitude of the summed
+        # terms, since per-leaf sums over rays cancel (sigma_max = 768 makes fp32 segment
+        # lengths the dominant error: ~2.5e-4 of each term)
+        bad = np.abs(a - b) > 1e-3 * sc + 1e-6 * np.abs(b).max()
+        assert not bad.any(), (tag, int(bad.sum()), float(np.abs(a - b).max()))
+    # leaves no ray touched stay exactly zero
+    mask = np.ones(gs.shape[0], bool)
+    mask[touched] = False
+    assert not gs[mask].any() and not gk[mask].any()

@@ -108,6 +108,16 @@ def test_color_derivative_is_weight(oracle_mod):
     np.testing.assert_allclose(gk[1, 0], g[0] * w1 * c[1] * (1 - c[1]) * Y0, rtol=1e-12)
 
 
+def test_scale_bounds_gradient(oracle_mod):
+    # the per-component magnitude of the summed terms bounds the sum (triangle inequality)
+    t = gen.scene_random(65, depth=4, sh_degree=2)
+    rays = gen.random_rays(66, 300)
+    g = rng(67).normal(size=(300, 3))
+    gs, gk, ss, sk = oracle_mod.backward(oracle_mod.OracleTree(t), rays, g, with_scale=True)
+    assert np.all(ss >= np.abs(gs) * (1 - 1e-12)) and np.all(sk >= np.abs(gk) * (1 - 1e-12))
+    assert ss.max() > 0 and sk.max() > 0
+
+
 def test_linear_in_dLdC(oracle_mod):
     t = gen.scene_random(61, depth=4, sh_degree=1)
     ot = oracle_mod.OracleTree(t)
