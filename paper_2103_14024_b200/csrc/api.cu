@@ -30,6 +30,8 @@ struct po_tree {
     int cam_cap = 0;
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
+    uint32_t root_entry = 0;       // device entry word of the root (traverse.cuh encoding)
+    bool node_masks = false;       // internal entries carry the child's occupancy mask
     // empty-space skipping grid (DevTree::macro): level M = min(5, D - 1)
     uint8_t* d_macro = nullptr;
     int macro_level = 0;
@@ -118,6 +120,9 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
 po::DevTree dev_tree(const po_tree* t) {
     po::DevTree d;
     d.child = t->d_child;
+    d.root_entry = t->root_entry;
+    d.node_masks = t->node_masks ? 1 : 0;
+    d.node_idx_mask = t->node_masks ? po::kMaskedIdx : po::kIdxMask;
     d.sigma = t->d_sigma;
     d.sh = t->d_sh;
     d.sh_row = t->sh_row;
@@ -322,7 +327,27 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
     e = cudaMemset(t->d_work, 0, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "memset(work)"));
-    e = cudaMemcpy(t->d_child, child, (size_t)n_nodes * 8 * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    {
+        // device child table: internal entries carry the child node's occupancy mask so the
+        // descent knows an empty octant without loading it (traverse.cuh, kMaskShift)
+        static const bool masks_off = [] {
+            const char* ev = getenv("PO_NODE_MASKS");
+            return ev && std::strcmp(ev, "0") == 0;
+        }();
+        t->node_masks = !masks_off && n_nodes <= ((int64_t)1 << po::kMaskShift);
+        std::vector<uint32_t> occ((size_t)n_nodes, 0);
+        for (int64_t i = 0; i < n_nodes; ++i)
+            for (int o = 0; o < 8; ++o) occ[i] |= (uint32_t)((child[i * 8 + o] >> 30) != po::kTagEmpty) << o;
+        std::vector<uint32_t> dev((size_t)n_nodes * 8);
+        for (size_t i = 0; i < dev.size(); ++i) {
+            const uint32_t en = child[i];
+            dev[i] = (t->node_masks && (en >> 30) == po::kTagInternal)
+                         ? (po::kTagInternal << 30) | (occ[en & po::kIdxMask] << po::kMaskShift) | (en & po::kIdxMask)
+                         : en;
+        }
+        t->root_entry = (po::kTagInternal << 30) | (t->node_masks ? occ[0] << po::kMaskShift : 0u);
+        e = cudaMemcpy(t->d_child, dev.data(), dev.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) return cleanup(cuda_status(e, "upload child"));
     if (n_leaves > 0) {
         e = cudaMemcpy(t->d_sigma, sigma, (size_t)n_leaves * sizeof(float), cudaMemcpyHostToDevice);

@@ -45,6 +45,58 @@ struct FwdVisitor {
     }
 };
 
+// Forward visitor that software-pipelines the leaf rows: early termination needs only
+// sigma~ and delta (T_{i+1} = T_i e^{-sigma delta}), so the 12 row loads of leaf i are issued
+// when the ray reaches it and consumed only at the next leaf (or at the end of the ray); their
+// latency overlaps the box steps in between.  fp32 payload only.
+template <int DEG>
+struct FwdVisitorPipe {
+    static constexpr int NE = 3 * ShDim<DEG>::B;
+    static constexpr int NV = (NE + 3) / 4;
+    const DevTree& tr;
+    float Y[ShDim<DEG>::B];
+    float T, gamma;
+    float C[3];
+    float4 row[NV];
+    float wpend;   // weight of the pending leaf (0: none)
+    __device__ FwdVisitorPipe(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g), wpend(0.f) {
+        sh_basis<DEG>(d, t.odd_sign, Y);
+        C[0] = C[1] = C[2] = 0.f;
+    }
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ void consume() {
+        float z[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const float vv[4] = {row[j].x, row[j].y, row[j].z, row[j].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int el = 4 * j + q;
+                if (el < NE) z[el % 3] = fmaf(vv[q], Y[el / 3], z[el % 3]);
+            }
+        }
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(wpend, sigmoidf_(z[ch]), C[ch]);
+    }
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        const float st = __ldg(tr.sigma + idx);
+        if (wpend != 0.f) consume();
+        wpend = 0.f;
+        if (!(st > 0.f)) return true;
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(tr.sh) + (size_t)idx * tr.sh_row);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) row[j] = __ldg(src + j);
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+        wpend = a.w;
+        T = a.Tn;
+        return !(T < gamma);
+    }
+    __device__ __forceinline__ void finish() {
+        if (wpend != 0.f) consume();
+        wpend = 0.f;
+    }
+};
+
 // Forward visitor whose leaf rows land in shared memory through cp.async (LDGSTS) instead of
 // 48 registers: the row loads stay fully in flight while the kernel fits 3 CTAs (24 warps)
 // per SM instead of 2.  Each thread owns a 208-B slot (52 words: conflict-free LDS.128).
@@ -338,12 +390,18 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                 if constexpr ((OPT & kOptSmemRow) != 0) {
                     extern __shared__ __align__(16) float po_dyn_smem[];
                     FwdVisitorSm<DEG, F16> v(tr, r.d, opt.gamma, po_dyn_smem + threadIdx.x * kStageWords);
-                    traverse<OPT & 3>(tr, r, v, stk);
+                    traverse<OPT & ~kOptSmemRow>(tr, r, v, stk);
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+                } else if constexpr ((OPT & kOptPipeRow) != 0 && !F16) {
+                    FwdVisitorPipe<DEG> v(tr, r.d, opt.gamma);
+                    traverse<OPT & ~kOptPipeRow>(tr, r, v, stk);
+                    v.finish();
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 } else {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                    traverse<OPT & 3>(tr, r, v, stk);
+                    traverse<OPT & (kOptLeafStep | kOptMacroSkip | kOptNodeMask)>(tr, r, v, stk);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -611,24 +669,26 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
-        return (v >= 0 && v <= 15) ? v : kRenderOptDefault;
+        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ? v : kRenderOptDefault;
     }();
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
     KFn fn = nullptr;
     int o = kRenderOptDefault;
     if (deg == 3 && !f16 && (minb != 2 || vopt != kRenderOptDefault)) {
-        // A/B instances: every variant at 2 CTAs/SM, the default variant at 1/3/4 CTAs/SM
-#define PO_R3(O0, O1, O2, O3) k_render<3, false, 2, O0>, k_render<3, false, 2, O1>, k_render<3, false, 2, O2>, \
-                              k_render<3, false, 2, O3>
-        static const KFn by_opt[16] = {PO_R3(0, 1, 2, 3), PO_R3(4, 5, 6, 7), PO_R3(8, 9, 10, 11),
-                                       PO_R3(12, 13, 14, 15)};
-#undef PO_R3
+        // A/B instances: each variant at 2 CTAs/SM, the default variant at 1/3/4 CTAs/SM
         static const KFn by_minb[4] = {k_render<3, false, 1, kRenderOptDefault>, nullptr,
                                        k_render<3, false, 3, kRenderOptDefault>,
                                        k_render<3, false, 4, kRenderOptDefault>};
         if (minb == 2) {
             o = vopt;
-            fn = by_opt[vopt];
+            switch (vopt) {
+                case 2: fn = k_render<3, false, 2, 2>; break;
+                case 4: fn = k_render<3, false, 2, 4>; break;
+                case 8: fn = k_render<3, false, 2, 8>; break;
+                case 16: fn = k_render<3, false, 2, 16>; break;
+                case 32: fn = k_render<3, false, 2, 32>; break;
+                default: fn = k_render<3, false, 2, 0>; break;
+            }
         } else {
             fn = by_minb[minb - 1];
         }

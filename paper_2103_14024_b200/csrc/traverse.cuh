@@ -27,9 +27,18 @@ namespace po {
 constexpr uint32_t kTagEmpty = 0u, kTagInternal = 1u, kTagLeaf = 2u;
 constexpr uint32_t kIdxMask = (1u << 30) - 1u;
 constexpr int kMaxDepth = 15;
+// Device child-table encoding (a0, po_tree_create).  Leaf entries: 2<<30 | leaf index (as in
+// the ABI).  Internal entries, when the tree has <= 2^22 nodes: 1<<30 | mask<<22 | node index,
+// mask = occupancy of that child node's 8 slots; otherwise the ABI encoding is kept and every
+// slot is treated as possibly occupied.
+constexpr int kMaskShift = 22;
+constexpr uint32_t kMaskedIdx = (1u << kMaskShift) - 1u;
 
 struct DevTree {
-    const uint32_t* __restrict__ child;   // [n_nodes][8]
+    const uint32_t* __restrict__ child;   // [n_nodes][8], device encoding (above)
+    uint32_t root_entry;                  // entry word of the root (index 0, its mask)
+    uint32_t node_idx_mask;               // kMaskedIdx or kIdxMask
+    int32_t node_masks;                   // 1 if internal entries carry child masks
     const float* __restrict__ sigma;      // [n_leaves]   sigma~
     const void* __restrict__ sh;          // [n_leaves][row] fp32 or fp16, rows 16-B aligned
     int32_t sh_row;                       // row stride in elements
@@ -106,15 +115,17 @@ struct SmemStack {
 // included) and vis.on_leaf(idx, t_in, t_out) for every positive-length leaf segment in
 // ray order; traversal stops when on_leaf returns false (early stop) or the ray exits.
 // Traversal variants (compile time, selected by measurement; see kernels.cu launch_render):
-//   kOptParentCache  register copy of the current level-(D-1) node's 8 child entries
 //   kOptLeafStep     fast neighbour step when the box is a single leaf-level cell
-constexpr int kOptParentCache = 1, kOptLeafStep = 2;
+//   (1 was a register copy of the leaf-parent's 8 entries: measured slower, removed)
+constexpr int kOptLeafStep = 2;
 constexpr int kOptSmemRow = 4;   // (render visitor) leaf rows staged in shared memory by cp.async
 // kOptMacroSkip: when the ray enters a level-M cell whose distance d to the nearest occupied
 // level-M cell is >= 1, jump in one step to the exit of the (2d-1)^3 block of level-M cells
 // around it (all empty by definition of d) instead of stepping through the empty octree
 // boxes one by one.  Leaves are never skipped, so the visited sequence is unchanged.
 constexpr int kOptMacroSkip = 8;
+constexpr int kOptPipeRow = 16;   // (render visitor) leaf rows consumed one leaf later (fp32)
+constexpr int kOptNodeMask = 32;  // skip the load of an empty octant using the entry's child mask
 // variant of the po_render kernel (po_render_stats / po_trace keep kOptDefault so their
 // internal-node counts stay the oracle's algorithm-independent "nodes met")
 constexpr int kRenderOptDefault = 0;
@@ -135,15 +146,9 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     int c[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) c[k] = min(max(cell_of(r.o[k], r.dg[k], t), 0), G - 1);
-    stk[0] = 0u;
+    stk[0] = tr.root_entry;
     int L = 0;
     vis.on_node();
-    // Register copy of the 8 child entries of the last node entered at level D-1 (the parents
-    // of leaf-level cells): one 32-B sector read by two LDG.128 when the ray enters such a
-    // node, after which stepping between its 2x2x2 cells needs no memory access at all.
-    uint32_t pnode = 0xFFFFFFFFu;
-    uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
-    const uint4* __restrict__ child4 = reinterpret_cast<const uint4*>(tr.child);
     bool check_macro = (OPT & kOptMacroSkip) != 0 && tr.macro != nullptr;
     while (true) {
         if constexpr ((OPT & kOptMacroSkip) != 0) {
@@ -189,28 +194,26 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
                 check_macro = false;   // occupied level-M cell: plain traversal until we leave it
             }
         }
-        uint32_t node = stk[L];
+        // stk[L] holds the device entry word of the node at level L; with occupancy masks the
+        // word carries the node's 8-bit child mask, so an empty octant is known without a load
+        uint32_t ent = stk[L];
         uint32_t e;
         int shift;
         while (true) {
             shift = D - 1 - L;
-            int oct = (((c[0] >> shift) & 1) << 2) | (((c[1] >> shift) & 1) << 1) | ((c[2] >> shift) & 1);
-            if ((OPT & kOptParentCache) && shift == 0) {
-                if (node != pnode) {
-                    pa = __ldg(child4 + 2u * node);
-                    pb = __ldg(child4 + 2u * node + 1u);
-                    pnode = node;
+            const int oct = (((c[0] >> shift) & 1) << 2) | (((c[1] >> shift) & 1) << 1) | ((c[2] >> shift) & 1);
+            if constexpr ((OPT & kOptNodeMask) != 0) {
+                const uint32_t m = tr.node_masks ? (ent >> kMaskShift) : 0xFFu;
+                if (!((m >> oct) & 1u)) {
+                    e = 0u;   // empty octant, known from the parent's entry word
+                    break;
                 }
-                const uint4 h = (oct & 4) ? pb : pa;
-                const uint32_t x0 = (oct & 1) ? h.y : h.x, x1 = (oct & 1) ? h.w : h.z;
-                e = (oct & 2) ? x1 : x0;
-            } else {
-                e = __ldg(tr.child + (node * 8u + (uint32_t)oct));   // n_nodes <= 2^29 (checked at upload)
             }
+            e = __ldg(tr.child + ((ent & tr.node_idx_mask) * 8u + (uint32_t)oct));
             if ((e >> 30) != kTagInternal) break;
-            node = e & kIdxMask;
+            ent = e;
             ++L;
-            stk[L] = node;
+            stk[L] = ent;
             vis.on_node();
         }
         // the box of entry e: level L+1, 2^shift leaf cells per axis.  Exit t per axis,
