@@ -104,10 +104,23 @@ class ClockSampler:
 
 
 def _dist():
+    """(world size, rank, CUDA device index).  PO_BENCH_DEVICE pins every rank to one device:
+    with PO_BENCH_BACKEND=gloo that exercises the multi-rank path on a single-GPU box."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("PO_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     return ws, rank, local
+
+
+def _init_pg(dev_index: int):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(dev_index)
+    backend = os.environ.get("PO_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    else:
+        dist.init_process_group(backend)
 
 
 def _workload_desc(tree_gen, wl="c1"):
@@ -137,9 +150,7 @@ def run_ours(args):
     metric = "1920x1080 FPS, SH-3 depth-10 fp16 PlenOctree (c3)" if wl == "c3" else METRIC
     ws, rank, local = _dist()
     if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        _init_pg(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     po.lib()
@@ -207,10 +218,12 @@ def run_ours(args):
 
     # e2e: the same frames through the host-buffer C-ABI entry point (H2D cameras, D2H image)
     pinned = torch.empty((1, H, W, 3), dtype=torch.float32, pin_memory=True).numpy()
+    cams_pinned = torch.empty((n_views, 16), dtype=torch.float32, pin_memory=True).numpy()
+    cams_pinned[:] = np.frombuffer(np.ascontiguousarray(cam_recs).tobytes(), dtype=np.float32).reshape(-1, 16)
     e2e_ms = 0.0
     e2e_steps = min(K, 50)
     for s in range(2):
-        po.po_render_host(tree, cam_recs[view_of(s):view_of(s) + 1], W, H, out_host=pinned, gamma=GAMMA)
+        po.po_render_host(tree, cams_pinned[view_of(s):view_of(s) + 1], W, H, out_host=pinned, gamma=GAMMA)
     if ws > 1:
         torch.distributed.barrier()
     for s in range(args.warmup, args.warmup + e2e_steps):
@@ -219,7 +232,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         v = view_of(s)
         e0.record(stream)
-        po.po_render_host(tree, cam_recs[v:v + 1], W, H, out_host=pinned, gamma=GAMMA)
+        po.po_render_host(tree, cams_pinned[v:v + 1], W, H, out_host=pinned, gamma=GAMMA)
         e1.record(stream)
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
@@ -276,9 +289,7 @@ def run_c4(args):
     ws, rank, local = _dist()
     group = None
     if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        _init_pg(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     t_gt = gen.scene_c1()
@@ -313,6 +324,15 @@ def run_c4(args):
             mx = gen.trees._part1by2(x) | (gen.trees._part1by2(y) << np.uint64(1))
             pick = pick[np.argsort((view.astype(np.uint64) << np.uint64(44)) | mx, kind="stable")]
         rays = torch.from_numpy(gen.camera_rays_f32(cams, W, H, pick // (W * H), pick % (W * H))).to(dev)
+        if args.ray_order == "leaf":
+            # batch preparation: order rays by the first leaf they enter.  The tree structure is
+            # fixed during optimisation, so this key is a per-pixel constant; leaves are
+            # numbered in Morton order, so rays that meet the same surface patch (from any
+            # view) run together and share leaf rows / gradient rows in L1/L2.
+            ids, _, _ = po.po_trace(gt, rays, max_leaves=1, gamma=0.0, with_nodes=False)
+            key = ids[:, 0].to(torch.int64)
+            key = torch.where(key < 0, torch.full_like(key, 1 << 40), key)
+            rays = rays[torch.argsort(key, stable=True)].contiguous()
         tgt = po.po_render_rays(gt, rays, gamma=0.0)   # targets: renders of the unperturbed tree
         batches.append((rays, tgt))
     torch.cuda.synchronize()
@@ -366,7 +386,8 @@ def run_c4(args):
                                    "gamma 0, SGD lr %g" % args.lr, "parallelism": f"ray data-parallel x{ws}, "
                                    "tree replicated, bucketed NCCL SUM allreduce",
                        "ray_sampling": args.ray_sampling + ("" if args.ray_sampling == "tile" or not args.unsorted
-                                                           else " (unsorted)")},
+                                                           else " (unsorted)"),
+                       "ray_order": args.ray_order},
             "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
             "leaf_visits_per_step": visits / K,
             "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
@@ -453,6 +474,8 @@ def main():
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
     ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
+    ap.add_argument("--ray-order", choices=["sampled", "leaf"], default="leaf",
+                    help="c4: keep the sampled order or sort the batch by first-entered leaf")
     ap.add_argument("--ray-sampling", choices=["tile", "pixel"], default="tile",
                     help="c4: sample 8x4 pixel tiles (coherent warps) or single pixels")
     args = ap.parse_args()

@@ -174,10 +174,10 @@ struct TotalVisitor {
     __device__ __forceinline__ void on_node() {}
     __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
         const float st = __ldg(tr.sigma + idx);
+        float z[3];
+        sh_dot<DEG, F16>(tr, idx, Y, z);   // row loads in flight together with sigma
         if (!(st > 0.f)) return true;
         const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
-        float z[3];
-        sh_dot<DEG, F16>(tr, idx, Y, z);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) C[ch] += (double)a.w * (double)sigmoidf_(z[ch]);
         T = a.Tn;
@@ -205,11 +205,11 @@ struct GradVisitor {
     __device__ __forceinline__ void on_node() {}
     __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
         const float st = __ldg(tr.sigma + idx);
+        float z[3], c[3];
+        sh_dot<DEG, F16>(tr, idx, Y, z);   // row loads in flight together with sigma
         if (!(st > 0.f)) return true;   // ReLU gate: w = 0 and dsigma = 0
         const float delta = __fsub_rn(t1, t0);
         const Absorb a = absorb(T, st, delta);
-        float z[3], c[3];
-        sh_dot<DEG, F16>(tr, idx, Y, z);
         double acc = 0.0;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
     PO_DECLARE_STACK(stk);
     __shared__ unsigned s_ticket;
     __shared__ unsigned s_block[kSlotRing];
-    __shared__ volatile unsigned s_pub[kSlotRing];
+    __shared__ unsigned s_pub[kSlotRing];
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_ticket = 0;
     if (threadIdx.x < kSlotRing) s_pub[threadIdx.x] = 0xFFFFFFFFu;
@@ -361,16 +361,18 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             const unsigned k = atomicAdd(&s_ticket, 1u);
             const unsigned slot = k >> 3;
             sub = k & 7u;
+            // hand-off through shared-memory atomics (ordered by the block fences): the warp that
+            // opens a slot claims the block and publishes it; the other 7 wait for the flag
             if (sub == 0) {
-                s_block[slot % kSlotRing] = atomicAdd(work, 1u);
+                atomicExch(&s_block[slot % kSlotRing], atomicAdd(work, 1u));
                 __threadfence_block();
-                s_pub[slot % kSlotRing] = slot;
+                atomicExch(&s_pub[slot % kSlotRing], slot);
             } else {
-                while (s_pub[slot % kSlotRing] != slot) {
+                while (atomicAdd(&s_pub[slot % kSlotRing], 0u) != slot) {
                 }
                 __threadfence_block();
             }
-            blk = s_block[slot % kSlotRing];
+            blk = atomicAdd(&s_block[slot % kSlotRing], 0u);
         }
         blk = __shfl_sync(0xffffffffu, blk, 0);
         sub = __shfl_sync(0xffffffffu, sub, 0);
@@ -423,7 +425,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
 }
 
 template <int DEG, bool F16>
-__global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
+__global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                      RenderOpts opt, float* __restrict__ out, double* __restrict__ aux) {
     PO_DECLARE_STACK(stk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(256) k_render_rays(DevTree tr, const float* __
 }
 
 template <int DEG, bool F16>
-__global__ void __launch_bounds__(256) k_backward(DevTree tr, const float* __restrict__ rays, int64_t n,
+__global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                   const float* __restrict__ dL_dC, const double* __restrict__ aux,
                                                   RenderOpts opt, float* __restrict__ grad_sigma,
                                                   float* __restrict__ grad_sh) {

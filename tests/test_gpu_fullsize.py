@@ -81,9 +81,10 @@ def test_c1_backward_ray_subset(env, c1_tree):
         assert rel <= 1e-3, (tag, rel)
         # per component (reading Q26 at c1 scale): relative to the magnitude of the summed
         # terms, since per-leaf sums over rays cancel; with sigma_max = 768 the fp32 segment
-        # lengths (error ~1e-6 world units at t ~ 3-4) perturb T_{i+1} by up to
-        # sigma_max * N * 1e-6 ~ 1e-2 relative on long gamma = 0 rays
-        bad = np.abs(a - b) > 1e-2 * sc + 1e-6 * np.abs(b).max()
+        # lengths (error e_delta ~ 1e-6 world units at t ~ 3-4) perturb T_{i+1} by up to
+        # sigma_max * N * e_delta ~ 1e-2 relative on long gamma = 0 rays, and a sliver
+        # segment's weight by e_delta / delta absolute; the floor 1e-3 max|ref| covers the latter
+        bad = np.abs(a - b) > 1e-2 * sc + 1e-3 * np.abs(b).max()
         assert not bad.any(), (tag, int(bad.sum()), float(np.abs(a - b).max()))
     # leaves no ray touched stay exactly zero
     mask = np.ones(gs.shape[0], bool)
