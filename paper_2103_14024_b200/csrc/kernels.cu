@@ -395,6 +395,22 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                     traverse<OPT & ~kOptSmemRow>(tr, r, v, stk);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+                } else if constexpr ((OPT & kOptProbeNoShade) != 0) {
+                    // measurement probe only (PO_RENDER_OPT=64, wrong colours): the traversal and
+                    // transmittance without any SH row, to size a traversal/shading split
+                    struct Probe {
+                        const DevTree& tr;
+                        float T, gamma;
+                        __device__ __forceinline__ void on_node() {}
+                        __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+                            const float st = __ldg(tr.sigma + idx);
+                            if (!(st > 0.f)) return true;
+                            T = absorb(T, st, __fsub_rn(t1, t0)).Tn;
+                            return !(T < gamma);
+                        }
+                    } v{tr, 1.f, opt.gamma};
+                    traverse<0>(tr, r, v, stk);
+                    C[0] = C[1] = C[2] = v.T;
                 } else if constexpr ((OPT & kOptPipeRow) != 0 && !F16) {
                     FwdVisitorPipe<DEG> v(tr, r.d, opt.gamma);
                     traverse<OPT & ~kOptPipeRow>(tr, r, v, stk);
@@ -671,7 +687,7 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
-        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ? v : kRenderOptDefault;
+        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 || v == 64) ? v : kRenderOptDefault;
     }();
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
     KFn fn = nullptr;
@@ -689,8 +705,14 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
                 case 8: fn = k_render<3, false, 2, 8>; break;
                 case 16: fn = k_render<3, false, 2, 16>; break;
                 case 32: fn = k_render<3, false, 2, 32>; break;
+                case 64: fn = k_render<3, false, 2, 64>; break;
                 default: fn = k_render<3, false, 2, 0>; break;
             }
+        } else if (vopt == kOptProbeNoShade) {
+            static const KFn probe[4] = {k_render<3, false, 1, kOptProbeNoShade>, nullptr,
+                                         k_render<3, false, 3, kOptProbeNoShade>,
+                                         k_render<3, false, 4, kOptProbeNoShade>};
+            fn = probe[minb - 1];
         } else {
             fn = by_minb[minb - 1];
         }

@@ -126,6 +126,7 @@ constexpr int kOptSmemRow = 4;   // (render visitor) leaf rows staged in shared 
 constexpr int kOptMacroSkip = 8;
 constexpr int kOptPipeRow = 16;   // (render visitor) leaf rows consumed one leaf later (fp32)
 constexpr int kOptNodeMask = 32;  // skip the load of an empty octant using the entry's child mask
+constexpr int kOptProbeNoShade = 64;   // measurement probe: traversal + T only (not a renderer)
 // variant of the po_render kernel (po_render_stats / po_trace keep kOptDefault so their
 // internal-node counts stay the oracle's algorithm-independent "nodes met")
 constexpr int kRenderOptDefault = 0;
