@@ -156,15 +156,16 @@ def run_ours(args):
     po.lib()
     t_gen = gen.scene_c3() if wl == "c3" else gen.scene_c1()
     tree = po.tree_from_gen(t_gen, payload=payload, device=local)
-    n_views = max(args.steps + args.warmup, 1) * ws
+    V = max(1, args.views_per_launch)
+    n_views = max(args.steps + args.warmup, 1) * ws * V
     cam_recs = np.concatenate([gen.config_camera(wl, v)[0] for v in range(n_views)])
     cams = po.cams_tensor(cam_recs, dev)
-    out = torch.empty((1, H, W, 3), dtype=torch.float32, device=dev)
+    out = torch.empty((V, H, W, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def view_of(step):
-        return (step * ws + rank) % n_views
+    def view_of(step):   # first of the V consecutive orbit views rank `rank` renders at `step`
+        return ((step * ws + rank) * V) % n_views
 
     # algorithmic bytes per launch: counters of the same traversal
     B = t_gen.basis_dim
@@ -173,15 +174,16 @@ def run_ours(args):
              "warp_boxes": 0}
     for s in range(args.warmup, args.warmup + args.steps):
         v = view_of(s)
-        st = po.po_render_stats(tree, cams[v:v + 1], W, H, gamma=GAMMA)
+        st = po.po_render_stats(tree, cams[v:v + V], W, H, gamma=GAMMA)
         for k in stats:
             stats[k] += st[k]
     K = max(args.steps, 1)
-    alg_bytes = (stats["leaf_visits"] * 4 + stats["sh_rows"] * row_bytes + stats["nodes"] * 32) / K + W * H * 12 + 64
+    alg_bytes = ((stats["leaf_visits"] * 4 + stats["sh_rows"] * row_bytes + stats["nodes"] * 32) / K
+                 + (W * H * 12 + 64) * V)
 
     for s in range(args.warmup):
         flush.zero_()
-        po.po_render(tree, cams[view_of(s):view_of(s) + 1], W, H, out=out, gamma=GAMMA)
+        po.po_render(tree, cams[view_of(s):view_of(s) + V], W, H, out=out, gamma=GAMMA)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -198,7 +200,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         v = view_of(s) if args.l2 != "same" else view_of(args.warmup)
         e0.record(stream)
-        po.po_render(tree, cams[v:v + 1], W, H, out=out, gamma=GAMMA)
+        po.po_render(tree, cams[v:v + V], W, H, out=out, gamma=GAMMA)
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
@@ -213,17 +215,17 @@ def run_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_per_step = t_max / K
-    fps = ws * K / (t_max / 1e3)
+    fps = ws * K * V / (t_max / 1e3)
     kernel_ms = t_ms / K   # one kernel launch per step
 
     # e2e: the same frames through the host-buffer C-ABI entry point (H2D cameras, D2H image)
-    pinned = torch.empty((1, H, W, 3), dtype=torch.float32, pin_memory=True).numpy()
+    pinned = torch.empty((V, H, W, 3), dtype=torch.float32, pin_memory=True).numpy()
     cams_pinned = torch.empty((n_views, 16), dtype=torch.float32, pin_memory=True).numpy()
     cams_pinned[:] = np.frombuffer(np.ascontiguousarray(cam_recs).tobytes(), dtype=np.float32).reshape(-1, 16)
     e2e_ms = 0.0
     e2e_steps = min(K, 50)
     for s in range(2):
-        po.po_render_host(tree, cams_pinned[view_of(s):view_of(s) + 1], W, H, out_host=pinned, gamma=GAMMA)
+        po.po_render_host(tree, cams_pinned[view_of(s):view_of(s) + V], W, H, out_host=pinned, gamma=GAMMA)
     if ws > 1:
         torch.distributed.barrier()
     for s in range(args.warmup, args.warmup + e2e_steps):
@@ -232,7 +234,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         v = view_of(s)
         e0.record(stream)
-        po.po_render_host(tree, cams_pinned[v:v + 1], W, H, out_host=pinned, gamma=GAMMA)
+        po.po_render_host(tree, cams_pinned[v:v + V], W, H, out_host=pinned, gamma=GAMMA)
         e1.record(stream)
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
@@ -240,7 +242,7 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_fps = ws * e2e_steps / (e2e_ms / 1e3)
+    e2e_fps = ws * e2e_steps * V / (e2e_ms / 1e3)
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -251,6 +253,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural SDF scene, seeded)",
             "config": _workload_desc(t_gen, wl) | {"parallelism": f"view-sharded x{ws}, tree replicated"}
+                      | ({"global_batch": f"{V} frames per rank per step (one launch)"} if V > 1 else {})
                       | ({"l2": f"NOT flushed ({args.l2}): analysis only"} if args.l2 != "flush" else {}),
             "mrays_per_s": round(fps * W * H / 1e6, 1),
             "leaf_visits_per_frame": stats["leaf_visits"] / K,
@@ -265,8 +268,8 @@ def run_ours(args):
                          "alg_bytes_def": f"leaf visits*4 B sigma + SH rows*{row_bytes} B + internal nodes met*32 B "
                                           "+ 12 B/pixel out",
                          "traffic_source": tsrc},
-            "e2e": {"value": round(e2e_fps, 2), "unit": UNIT, "h2d_bytes_per_step": 64,
-                    "d2h_bytes_per_step": W * H * 12, "entry": "po_render_host (host cameras -> host image)"},
+            "e2e": {"value": round(e2e_fps, 2), "unit": UNIT, "h2d_bytes_per_step": 64 * V,
+                    "d2h_bytes_per_step": W * H * 12 * V, "entry": "po_render_host (host cameras -> host image)"},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -468,6 +471,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["c1", "c3", "c4"], default="c1")
+    ap.add_argument("--views-per-launch", type=int, default=1,
+                    help="render V consecutive orbit views per po_render launch (c2-style batches)")
     ap.add_argument("--l2", choices=["flush", "orbit", "same"], default="flush",
                     help="analysis only: 'orbit' = consecutive orbit views without flushing (warm, realistic "
                          "frame-to-frame reuse), 'same' = one view repeated; the reported number uses 'flush'")

@@ -168,6 +168,13 @@ po_status po_trace(const po_tree* tree, const float* rays, int64_t n, const po_r
 po_status po_render_stats(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                           const po_render_opts* opts, unsigned long long* counters, po_stream stream);
 
+/* po_render_timeline: po_render that also records, for every 8x4-pixel warp tile, device
+ * uint64 timeline[ceil(W/16)*ceil(H/16)*n_cams*8][4] = {globaltimer ns at tile start, at tile
+ * end, SM id << 32 | block index in its view, view} (scheduling analysis; same image). */
+po_status po_render_timeline(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                             const po_render_opts* opts, float* out_rgb, unsigned long long* timeline,
+                             po_stream stream);
+
 /* Number of kernel launches the library has issued since load (bench accounting). */
 int64_t po_launch_count(void);
 

@@ -26,7 +26,8 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_destroy", "po_tree_info",
            "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward",
-           "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats"]
+           "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
+           "po_render_timeline"]
 
 
 class PoError(RuntimeError):
@@ -73,6 +74,7 @@ def lib():
         L.po_tree_sgd_step_range.argtypes = [P, P, P, F, I64, I64, P]
         L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, P]
         L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
+        L.po_render_timeline.argtypes = [P, P, I32, I32, I32, P, P, P, P]
         for name in EXPORTS:
             if name not in ("po_last_error", "po_version", "po_launch_count"):
                 getattr(L, name).restype = ctypes.c_int
@@ -299,6 +301,20 @@ def po_render_stats(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.01,
     v = ctr.cpu().tolist()
     return dict(leaf_visits=v[0], sh_rows=v[1], nodes=v[2], hit_rays=v[3], boxes=v[4], leaf_level_boxes=v[5],
                 warp_boxes=v[6])
+
+
+def po_render_timeline(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
+                       stream=None):
+    """po_render plus one (t_start_ns, t_end_ns, smid<<32|block, view) record per warp tile."""
+    import torch
+    cams = _need(cams, torch.float32, (16,))
+    n = cams.shape[0]
+    out = torch.empty((n, H, W, 3), dtype=torch.float32, device=cams.device)
+    tl = torch.zeros((((W + 15) // 16) * ((H + 15) // 16) * n * 8, 4), dtype=torch.int64, device=cams.device)
+    o = _opts(gamma, background)
+    _check(lib().po_render_timeline(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), _ptr(out), _ptr(tl),
+                                    _stream(stream)))
+    return out, tl
 
 
 def launch_count() -> int:

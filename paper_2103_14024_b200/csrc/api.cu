@@ -44,7 +44,8 @@ struct po_tree {
     static constexpr int kWorkSlots = 64;
     unsigned* d_work = nullptr;
     std::atomic<uint32_t> work_rr{0};
-    unsigned* next_work() { return d_work + 2 * (work_rr.fetch_add(1) % kWorkSlots); }
+    int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
+    unsigned* work_of(int slot) { return d_work + 2 * slot; }
 };
 
 namespace {
@@ -446,6 +447,20 @@ static po_status check_cams_host(const po_camera* c, int32_t n) {
     return PO_OK;
 }
 
+// Block hand-out order (centre-out, block_order) and launch of the persistent render kernel.
+// (An order by measured or probed block cost was tried in r01 and was slower: DESIGN.md §6.1.)
+static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams, int W, int H,
+                                  const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
+                                  unsigned long long* timeline = nullptr) {
+    cudaError_t e = cudaSuccess;
+    const unsigned* order = block_order(t, W, H, s, &e);
+    if (e != cudaSuccess) return cuda_status(e, "block order");
+    const int slot = t->next_slot();
+    return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
+                                      out, t->work_of(slot), order, timeline, s),
+                    where);
+}
+
 po_status po_render(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                     const po_render_opts* opts, float* out_rgb, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
@@ -457,12 +472,7 @@ po_status po_render(const po_tree* t, const po_camera* cams, int32_t n_cams, int
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     po_tree* tm = const_cast<po_tree*>(t);   // only scratch (work counters, block order) is mutated
-    cudaError_t oe;
-    const unsigned* order = block_order(tm, W, H, (cudaStream_t)stream, &oe);
-    if (oe != cudaSuccess) return cuda_status(oe, "block order");
-    return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
-                                      out_rgb, tm->next_work(), order, (cudaStream_t)stream),
-                    "po_render");
+    return render_scheduled(tm, cams, n_cams, W, H, o, out_rgb, (cudaStream_t)stream, "po_render");
 }
 
 po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
@@ -499,11 +509,7 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
         if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(image)");
         t->img_cap = out_bytes;
     }
-    const unsigned* order = block_order(t, W, H, s, &e);
-    if (e != cudaSuccess) return cuda_status(e, "block order");
-    po_status st = launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, t->d_cams,
-                                              n_cams, W, H, o, t->d_img, t->next_work(), order, s),
-                            "po_render_host");
+    po_status st = render_scheduled(t, t->d_cams, n_cams, W, H, o, t->d_img, s, "po_render_host");
     if (st == PO_OK) {
         e = cudaMemcpyAsync(out_host, t->d_img, out_bytes, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) st = cuda_status(e, "D2H image");
@@ -599,6 +605,21 @@ po_status po_trace(const po_tree* t, const float* rays, int64_t n, const po_rend
     return launched(po::launch_trace(dev_tree(t), rays, n, o.gamma, max_leaves, max_leaves > 0 ? leaf_ids : nullptr,
                                      counts, node_counts, (cudaStream_t)stream),
                     "po_trace");
+}
+
+po_status po_render_timeline(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                             const po_render_opts* opts, float* out_rgb, unsigned long long* timeline,
+                             po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    if (po_status s = check_image(n_cams, W, H)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n_cams == 0) return PO_OK;
+    if (!cams || !out_rgb || !timeline) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return render_scheduled(const_cast<po_tree*>(t), cams, n_cams, W, H, o, out_rgb, (cudaStream_t)stream,
+                            "po_render_timeline", timeline);
 }
 
 po_status po_render_stats(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,

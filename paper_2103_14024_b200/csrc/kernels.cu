@@ -343,7 +343,8 @@ constexpr int kSlotRing = 16;
 template <int DEG, bool F16, int MINB, int OPT>
 __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camera* __restrict__ cams, int n_cams, int W,
                                                 int H, RenderOpts opt, float* __restrict__ out,
-                                                unsigned* __restrict__ work, const unsigned* __restrict__ order) {
+                                                unsigned* __restrict__ work, const unsigned* __restrict__ order,
+                                                unsigned long long* __restrict__ timeline) {
     PO_DECLARE_STACK(stk);
     __shared__ unsigned s_ticket;
     __shared__ unsigned s_block[kSlotRing];
@@ -368,8 +369,10 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                 __threadfence_block();
                 atomicExch(&s_pub[slot % kSlotRing], slot);
             } else {
-                while (atomicAdd(&s_pub[slot % kSlotRing], 0u) != slot) {
-                }
+                // sleep while waiting: a busy spin starves the publishing warp, because the
+                // scheduler prefers higher warp ids (r01 timeline: 7 of 8 warps idled ~30 us
+                // at the start of every launch)
+                while (atomicAdd(&s_pub[slot % kSlotRing], 0u) != slot) __nanosleep(64);
                 __threadfence_block();
             }
             blk = atomicAdd(&s_block[slot % kSlotRing], 0u);
@@ -379,7 +382,9 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         if (blk >= total) break;
         const unsigned view = blk / per_view;
         unsigned rem = blk - view * per_view;
-        if (order != nullptr) rem = __ldg(order + rem);   // centre-out block order (see launch_render)
+        if (order != nullptr) rem = __ldg(order + rem);   // block hand-out order (see launch_render)
+        unsigned long long t_tile = 0;
+        if (timeline != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_tile));
         const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
         const int px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
         const int py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 } else {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                    traverse<OPT & (kOptLeafStep | kOptMacroSkip | kOptNodeMask)>(tr, r, v, stk);
+                    traverse<OPT & (kOptLeafStep | kOptMacroSkip | kOptNodeMask | kOptLean)>(tr, r, v, stk);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -428,6 +433,21 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             p[0] = C[0];
             p[1] = C[1];
             p[2] = C[2];
+        }
+        if (timeline != nullptr) {   // measurement mode (po_render_timeline): one record per warp tile
+            __syncwarp();
+            if (lane == 0) {
+                unsigned long long t1;
+                unsigned sm32;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(sm32));
+                const unsigned long long sm = sm32;
+                unsigned long long* rec = timeline + 4 * ((size_t)blk * 8 + sub);
+                rec[0] = t_tile;
+                rec[1] = t1;
+                rec[2] = (sm << 32) | rem;
+                rec[3] = view;
+            }
         }
     }
     __syncthreads();
@@ -672,7 +692,7 @@ static int persistent_grid(K kernel, int64_t max_ctas, size_t dyn_smem = 0) {
 
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
                           const RenderOpts& opt, float* out, unsigned* work, const unsigned* order,
-                          cudaStream_t s) {
+                          unsigned long long* timeline, cudaStream_t s) {
     const int64_t tiles = (int64_t)((W + 7) / 8) * ((H + 3) / 4) * n_cams;
     if (tiles >= (int64_t)0xFFFFFFF0u) return cudaErrorInvalidValue;
     // CTAs per SM the register budget is tuned for.  Default 2 (<= 128 registers): all 12
@@ -687,9 +707,11 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
-        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 || v == 64) ? v : kRenderOptDefault;
+        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128) ? v
+                                                                                                      : kRenderOptDefault;
     }();
-    using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*);
+    using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
+                         unsigned long long*);
     KFn fn = nullptr;
     int o = kRenderOptDefault;
     if (deg == 3 && !f16 && (minb != 2 || vopt != kRenderOptDefault)) {
@@ -706,6 +728,7 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
                 case 16: fn = k_render<3, false, 2, 16>; break;
                 case 32: fn = k_render<3, false, 2, 32>; break;
                 case 64: fn = k_render<3, false, 2, 64>; break;
+                case 128: fn = k_render<3, false, 2, 128>; break;
                 default: fn = k_render<3, false, 2, 0>; break;
             }
         } else if (vopt == kOptProbeNoShade) {
@@ -730,7 +753,7 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
         grid = it->second;
     }
     const int g = (int)((int64_t)grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8);
-    fn<<<g, 256, dyn, s>>>(tr, cams, n_cams, W, H, opt, out, work, order);
+    fn<<<g, 256, dyn, s>>>(tr, cams, n_cams, W, H, opt, out, work, order, timeline);
     return cudaGetLastError();
 }
 

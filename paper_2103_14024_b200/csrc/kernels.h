@@ -16,9 +16,11 @@ struct RenderOpts {
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.
 // order: NULL (raster) or a device permutation of the ceil(W/16)*ceil(H/16) blocks of a view
 // giving the order in which blocks are handed out.
+// timeline: NULL, or device uint64[n_blocks * 8][4] receiving one record per warp tile
+// (globaltimer start, end, smid << 32 | block, view) -- measurement mode of po_render_timeline.
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
                           const RenderOpts& opt, float* out, unsigned* work, const unsigned* order,
-                          cudaStream_t s);
+                          unsigned long long* timeline, cudaStream_t s);
 cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, float* rays, cudaStream_t s);
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
                                const RenderOpts& opt, float* out, double* aux, cudaStream_t s);

@@ -127,6 +127,7 @@ constexpr int kOptMacroSkip = 8;
 constexpr int kOptPipeRow = 16;   // (render visitor) leaf rows consumed one leaf later (fp32)
 constexpr int kOptNodeMask = 32;  // skip the load of an empty octant using the entry's child mask
 constexpr int kOptProbeNoShade = 64;   // measurement probe: traversal + T only (not a renderer)
+constexpr int kOptLean = 128;          // leaner neighbour step (see traverse)
 // variant of the po_render kernel (po_render_stats / po_trace keep kOptDefault so their
 // internal-node counts stay the oracle's algorithm-independent "nodes met")
 constexpr int kRenderOptDefault = 0;
@@ -240,7 +241,20 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         t = texit;
         int nc[3];
         bool out = false;
-        if ((OPT & kOptLeafStep) && size == 1) {
+        if constexpr ((OPT & kOptLean) != 0) {
+            // leaner step: every axis whose face is crossed at texit steps (an exact edge or
+            // corner crossing moves diagonally), the others are point-located with one F2I.FLOOR
+            // (an exactly integral coordinate while moving down yields a zero-length box that
+            // the `tout > t` test skips) and clamped into the box
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const bool hit = te[k] == texit;
+                const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;
+                const int ck = __float2int_rd(fmaf(t, r.dg[k], r.o[k]));
+                nc[k] = hit ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
+                out |= hit & ((unsigned)nex >= (unsigned)G);
+            }
+        } else if ((OPT & kOptLeafStep) && size == 1) {
             // leaf-level box (the common step): the other two coordinates cannot change
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
