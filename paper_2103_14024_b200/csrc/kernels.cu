@@ -357,28 +357,32 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
     const unsigned per_view = bx_n * by_n;
     const unsigned total = per_view * (unsigned)n_cams;
     while (true) {
-        unsigned blk = 0, sub = 0;
-        if (lane == 0) {
-            const unsigned k = atomicAdd(&s_ticket, 1u);
-            const unsigned slot = k >> 3;
-            sub = k & 7u;
-            // hand-off through shared-memory atomics (ordered by the block fences): the warp that
-            // opens a slot claims the block and publishes it; the other 7 wait for the flag
-            if (sub == 0) {
+        // hand-off through shared-memory atomics (ordered by the block fences): the warp that
+        // opens a slot claims the block and publishes it; the other 7 wait for the flag.  The
+        // control flow is warp-uniform (lane 0 does the atomics, every branch decision is
+        // shuffled to the whole warp), and waiting warps sleep between polls.
+        unsigned k = 0;
+        if (lane == 0) k = atomicAdd(&s_ticket, 1u);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        const unsigned slot = k >> 3, sub = k & 7u;
+        if (sub == 0) {
+            if (lane == 0) {
                 atomicExch(&s_block[slot % kSlotRing], atomicAdd(work, 1u));
                 __threadfence_block();
                 atomicExch(&s_pub[slot % kSlotRing], slot);
-            } else {
-                // sleep while waiting: a busy spin starves the publishing warp, because the
-                // scheduler prefers higher warp ids (r01 timeline: 7 of 8 warps idled ~30 us
-                // at the start of every launch)
-                while (atomicAdd(&s_pub[slot % kSlotRing], 0u) != slot) __nanosleep(64);
-                __threadfence_block();
             }
-            blk = atomicAdd(&s_block[slot % kSlotRing], 0u);
+        } else {
+            while (true) {
+                unsigned p = 0;
+                if (lane == 0) p = atomicAdd(&s_pub[slot % kSlotRing], 0u);
+                if (__shfl_sync(0xffffffffu, p, 0) == slot) break;
+                __nanosleep(64);
+            }
+            __threadfence_block();
         }
+        unsigned blk = 0;
+        if (lane == 0) blk = atomicAdd(&s_block[slot % kSlotRing], 0u);
         blk = __shfl_sync(0xffffffffu, blk, 0);
-        sub = __shfl_sync(0xffffffffu, sub, 0);
         if (blk >= total) break;
         const unsigned view = blk / per_view;
         unsigned rem = blk - view * per_view;
