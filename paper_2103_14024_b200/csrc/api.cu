@@ -31,6 +31,9 @@ struct po_tree {
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
     uint32_t root_entry = 0;       // device entry word of the root (traverse.cuh encoding)
+    uint32_t* d_child_b = nullptr; // child table whose level-(D-2) targets are brick indices
+    uint32_t* d_brick = nullptr;   // [n_bricks][64] flattened bottom two levels
+    uint32_t brick_root = 0;
     bool node_masks = false;       // internal entries carry the child's occupancy mask
     // empty-space skipping grid (DevTree::macro): level M = min(5, D - 1)
     uint8_t* d_macro = nullptr;
@@ -131,6 +134,9 @@ po::DevTree dev_tree(const po_tree* t) {
     for (int k = 0; k < 3; ++k) d.bmin[k] = t->desc.bbox_min[k];
     d.scale = (float)std::ldexp(1.0, t->desc.max_depth) / t->desc.bbox_edge;
     d.odd_sign = t->desc.sh_sign == PO_SH_NO_CS ? -1.f : 1.f;
+    d.child_b = t->d_child_b;
+    d.brick = t->d_brick;
+    d.brick_root = t->brick_root;
     d.macro = t->d_macro;
     d.macro_shift = t->desc.max_depth - t->macro_level;
     d.macro_n = 1 << t->macro_level;
@@ -348,6 +354,52 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
         }
         t->root_entry = (po::kTagInternal << 30) | (t->node_masks ? occ[0] << po::kMaskShift : 0u);
         e = cudaMemcpy(t->d_child, dev.data(), dev.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+        // bricks (opt-in experiment, PO_BRICKS=1; measured slower): each
+        // level-(D-2) node gets a 4x4x4 brick of its leaf-level cells
+        static const bool bricks_on = [] {
+            const char* ev = getenv("PO_BRICKS");
+            return ev && std::strcmp(ev, "1") == 0;
+        }();
+        const int Lb = D - 2;
+        if (e == cudaSuccess && bricks_on && Lb >= 0 && n_leaves <= (int64_t)po::kBrickLeafBit) {
+            const uint32_t idx_mask = t->node_masks ? po::kMaskedIdx : po::kIdxMask;
+            std::vector<uint32_t> bid((size_t)n_nodes, 0xFFFFFFFFu);
+            uint32_t nb = 0;
+            for (int64_t i = 0; i < n_nodes; ++i)
+                if (node_level[(size_t)i] == Lb) bid[(size_t)i] = nb++;
+            std::vector<uint32_t> brick((size_t)nb * 64, 0);
+            for (int64_t i = 0; i < n_nodes; ++i) {
+                if (bid[(size_t)i] == 0xFFFFFFFFu) continue;
+                uint32_t* b = brick.data() + (size_t)bid[(size_t)i] * 64;
+                for (int o1 = 0; o1 < 8; ++o1) {
+                    const uint32_t e1 = child[i * 8 + o1];
+                    const int x1 = (o1 >> 2) & 1, y1 = (o1 >> 1) & 1, z1 = o1 & 1;
+                    for (int o2 = 0; o2 < 8; ++o2) {
+                        const int x = 2 * x1 + ((o2 >> 2) & 1), y = 2 * y1 + ((o2 >> 1) & 1), z = 2 * z1 + (o2 & 1);
+                        uint32_t v;
+                        if ((e1 >> 30) == po::kTagEmpty)
+                            v = 3u << 30;   // empty level-(D-1) box
+                        else if ((e1 >> 30) == po::kTagLeaf)
+                            v = (3u << 30) | po::kBrickLeafBit | (e1 & po::kIdxMask);   // one coarser leaf
+                        else
+                            v = child[(size_t)(e1 & po::kIdxMask) * 8 + o2];   // leaf-level leaf or empty
+                        b[x * 16 + y * 4 + z] = v;
+                    }
+                }
+            }
+            std::vector<uint32_t> devb(dev);
+            for (size_t j = 0; j < devb.size(); ++j) {
+                const uint32_t en = child[j];
+                if ((en >> 30) == po::kTagInternal && bid[en & po::kIdxMask] != 0xFFFFFFFFu)
+                    devb[j] = (devb[j] & ~idx_mask) | bid[en & po::kIdxMask];
+            }
+            t->brick_root = Lb == 0 ? ((po::kTagInternal << 30) | bid[0]) : t->root_entry;
+            if ((e = cudaMalloc(&t->d_child_b, devb.size() * sizeof(uint32_t))) == cudaSuccess &&
+                (e = cudaMalloc(&t->d_brick, std::max<size_t>(brick.size(), 1) * sizeof(uint32_t))) == cudaSuccess &&
+                (e = cudaMemcpy(t->d_child_b, devb.data(), devb.size() * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice)) == cudaSuccess && !brick.empty())
+                e = cudaMemcpy(t->d_brick, brick.data(), brick.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+        }
     }
     if (e != cudaSuccess) return cleanup(cuda_status(e, "upload child"));
     if (n_leaves > 0) {
@@ -389,6 +441,8 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_img) cudaFree(t->d_img);
     if (t->d_order) cudaFree(t->d_order);
     if (t->d_macro) cudaFree(t->d_macro);
+    if (t->d_child_b) cudaFree(t->d_child_b);
+    if (t->d_brick) cudaFree(t->d_brick);
     t->d_child = nullptr;
     delete t;
     return PO_OK;

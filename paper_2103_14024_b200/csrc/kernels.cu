@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 } else {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                    traverse<OPT & (kOptLeafStep | kOptMacroSkip | kOptNodeMask | kOptLean)>(tr, r, v, stk);
+                    traverse<OPT & (kOptLeafStep | kOptMacroSkip | kOptNodeMask | kOptLean | kOptBrick)>(tr, r, v, stk);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -701,8 +701,9 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     if (tiles >= (int64_t)0xFFFFFFF0u) return cudaErrorInvalidValue;
     // CTAs per SM the register budget is tuned for.  Default 2 (<= 128 registers): all 12
     // LDG.128 of a leaf row stay in flight, which beat 3-4 CTAs/SM on B200 (r01: 4127 vs 3819
-    // vs 3160 FPS on c1).  For the SH-3 fp32 path PO_RENDER_MINB=1..4 and PO_RENDER_OPT=0..3
-    // (traversal variants, traverse.cuh) select other instances for A/B experiments.
+    // vs 3160 FPS on c1).  For the SH-3 fp32 path PO_RENDER_MINB=1..4 and PO_RENDER_OPT
+    // (traversal variant bits, traverse.cuh; 0 = the plain step, 256/384 need PO_BRICKS=1)
+    // select other instances for A/B experiments.
     static const int minb = [] {
         const char* e = getenv("PO_RENDER_MINB");
         const int v = e ? atoi(e) : 2;
@@ -711,7 +712,8 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
-        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128) ? v
+        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128 || v == 256 ||
+                v == 384) ? v
                                                                                                       : kRenderOptDefault;
     }();
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
@@ -733,6 +735,8 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
                 case 32: fn = k_render<3, false, 2, 32>; break;
                 case 64: fn = k_render<3, false, 2, 64>; break;
                 case 128: fn = k_render<3, false, 2, 128>; break;
+                case 256: fn = tr.brick ? k_render<3, false, 2, 256> : k_render<3, false, 2, 0>; break;
+                case 384: fn = tr.brick ? k_render<3, false, 2, 384> : k_render<3, false, 2, 128>; break;
                 default: fn = k_render<3, false, 2, 0>; break;
             }
         } else if (vopt == kOptProbeNoShade) {
