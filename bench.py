@@ -340,7 +340,7 @@ def run_c4(args):
         batches.append((rays, tgt))
     torch.cuda.synchronize()
     gt.destroy()
-    opt = OctreeOptimizer(tree, lr=args.lr, gamma=0.0, device=dev)
+    opt = OctreeOptimizer(tree, lr=args.lr, gamma=0.0, device=dev, chunks=args.chunks, max_seg=args.max_seg)
     # algorithmic bytes of the dominant kernel (k_backward, pass 2 with aux) over the timed batches
     visits = nodes = 0
     for rays, _ in batches[args.warmup:]:
@@ -390,7 +390,9 @@ def run_c4(args):
                                    "tree replicated, bucketed NCCL SUM allreduce",
                        "ray_sampling": args.ray_sampling + ("" if args.ray_sampling == "tile" or not args.unsorted
                                                            else " (unsorted)"),
-                       "ray_order": args.ray_order},
+                       "ray_order": args.ray_order, "pass2_chunks": opt.n_chunks(),
+                       "pass2": (f"stored segments (max {args.max_seg}/ray, {args.max_seg * n_rays * 32 / 2**30:.1f} GiB)"
+                                 if args.max_seg > 0 else "re-traversal")},
             "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
             "leaf_visits_per_step": visits / K,
             "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
@@ -477,6 +479,10 @@ def main():
                     help="analysis only: 'orbit' = consecutive orbit views without flushing (warm, realistic "
                          "frame-to-frame reuse), 'same' = one view repeated; the reported number uses 'flush'")
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
+    ap.add_argument("--max-seg", type=int, default=256,
+                    help="c4: stored pass-1 segments per ray (0 = pass 2 re-traverses every ray)")
+    ap.add_argument("--chunks", type=int, default=None,
+                    help="c4: pass-2 chunks overlapped with the allreduce (default 8 if N>1, else 1)")
     ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
     ap.add_argument("--ray-order", choices=["sampled", "leaf"], default="leaf",

@@ -113,28 +113,90 @@ po_status po_render_host(const po_tree* tree, const po_camera* cams_host, int32_
 po_status po_camera_rays(const po_camera* cams, int32_t n_cams, int32_t W, int32_t H, float* rays, int32_t device,
                          po_stream stream);
 
+/* Stored pass-1 segments (optional, training path).  The paper's pass 2 re-traverses every
+ * ray to recover the per-segment weights; with 180 GB of HBM per GPU the forward
+ * can instead store, for every sigma~ > 0 segment i it composites, the values pass 2 needs:
+ *   record (k, ray r) = 8 floats at records + (k * n_rays + r) * 8 (segment-major, so the
+ *   lanes of a warp touch adjacent records):
+ *   (leaf index as uint32 bits, delta_i, w_i, T_{i+1}, c_r, c_g, c_b, 0)
+ *   count[r] = number of sigma~ > 0 segments, or max_seg + 1 if they did not fit (pass 2 then
+ *   re-traverses that ray, so any max_seg >= 0 is exact).
+ * Pass 2 replays the records through the same arithmetic as the re-traversal: the gradients
+ * are identical up to the order of the atomic sums.  Memory: max_seg * n_rays * 32 B
+ * (c4: 192 x 1 M rays = 6.4 GB), caller-owned, 16-byte aligned. */
+typedef struct {
+    float* records;     /* device float[max_seg][n_rays][8] */
+    int32_t* count;     /* device int32[n_rays] */
+    int64_t n_rays;     /* batch size the buffer is laid out for */
+    int32_t max_seg;
+} po_segments;
+
 /* Forward render of explicit rays.
- * rays     device float[n][6] = (origin xyz, direction xyz); the direction is normalised
- *          by the library (zero direction => that ray returns the background).
- * out_rgb  device float[n][3]
- * aux      device double[n][4] or NULL: (C_r, C_g, C_b, T_final) accumulated in double;
- *          po_render_backward uses it to skip its own first pass. */
+ * rays       device float[n][6] = (origin xyz, direction xyz); the direction is normalised
+ *            by the library (zero direction => that ray returns the background).
+ * out_rgb    device float[n][3]
+ * aux        device double[n][4] or NULL: (C_r, C_g, C_b, T_final) accumulated in double;
+ *            po_render_backward uses it to skip its own first pass.
+ * leaf_span  device uint32[n][2] or NULL (needs aux, 8-byte aligned): the smallest and
+ *            largest index of the sigma~ > 0 leaves the ray composited -- exactly the leaves
+ *            its backward writes (P:961-963 gates the rest) -- or (0xFFFFFFFF, 0) for none.
+ *            Input of po_backward_plan (SURVEY 8(e) overlap of pass 2 with the allreduce).
+ * segments   NULL or a po_segments buffer with n_rays == n (needs aux): written for pass 2. */
 po_status po_render_rays(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
-                         float* out_rgb, double* aux, po_stream stream);
+                         float* out_rgb, double* aux, uint32_t* leaf_span, const po_segments* segments,
+                         po_stream stream);
 
 /* ---- a7/a8: analytic backward (App. B.3: P:886-892 colour, P:938-947 density,
  * P:949-957 two passes, P:959-963 ReLU) -----------------------------------------------
  * dL_dC       device float[n][3], the loss gradient per ray (e.g. 2(C^ - C) for Eq. 3).
  * aux         device double[n][4] from po_render_rays with the same tree/rays/opts, or NULL
  *             (then the kernel runs its own first pass to get the total sum_k c_k w_k).
+ * segments    NULL, or the po_segments that same po_render_rays call wrote (needs aux):
+ *             rays whose segments fit are replayed without traversal.
  * grad_sigma  device float[n_leaves]      d L / d sigma~   (ACCUMULATED: +=)
  * grad_sh     device float[n_leaves][B][3] d L / d k         (ACCUMULATED: +=)
  * The caller zeroes the gradients; cross-ray summation order is nondeterministic.
  * opts->gamma applies exactly as in the forward (gamma = 0 is the paper-literal optimiser,
  * reading Q12). */
 po_status po_render_backward(const po_tree* tree, const float* rays, int64_t n, const float* dL_dC,
-                             const double* aux, const po_render_opts* opts, float* grad_sigma, float* grad_sh,
-                             po_stream stream);
+                             const double* aux, const po_segments* segments, const po_render_opts* opts,
+                             float* grad_sigma, float* grad_sh, po_stream stream);
+
+/* ---- a8/a9 overlap: pass 2 in K chunks whose gradient ranges become final in order ------
+ * Leaves are numbered depth first, so each subtree is a contiguous index range (a0).  Given
+ * leaf bounds b_0 <= ... <= b_{K-1} = n_leaves, chunk j holds the rays whose lowest sigma~>0
+ * leaf index lies in [b_{j-1}, b_j) (b_{-1} = 0).  A ray writes no leaf below that index
+ * (P:961-963 gates sigma~ <= 0 leaves to zero), so once chunks 0..j have run the gradient of
+ * leaves [0, b_j) is FINAL: its allreduce + SGD can start while chunks j+1.. run.
+ * Rays with no sigma~>0 leaf write nothing and are in no chunk.
+ *
+ * po_backward_plan
+ *   leaf_span      device uint32[n][2] from po_render_rays (same tree, rays, opts)
+ *   K              1..64 chunks
+ *   leaf_bounds    host int64[K] or NULL (then b_j = floor(n_leaves (j+1) / K)); must be
+ *                  non-decreasing with b_{K-1} = n_leaves, else PO_ERR_INVALID_ARG
+ *   perm           device int32[n] out: ray indices sorted by lowest leaf (stable, so the
+ *                  caller's ray order is kept inside a key); n < 2^31
+ *   chunk_ray_end  device int64[K] out: chunk j = perm[chunk_ray_end[j-1] .. chunk_ray_end[j])
+ *   leaf_end       host int64[K] out or NULL: the bounds b_j used (known without a device sync)
+ *   key_quantiles  device int64[K] out or NULL: bounds that would split THIS batch's rays into
+ *                  K equal chunks (last = n_leaves); a caller may feed them back as the next
+ *                  step's leaf_bounds (batches of one scene have similar distributions)
+ * Stream-ordered; uses sort scratch cached in the tree, so plans on one tree must not run
+ * concurrently on different streams.  The chunk bounds stay on the device: the chunks are
+ * launched without waiting for the plan.
+ *
+ * po_render_backward_chunk: po_render_backward over chunk `chunk` of a plan (rays, dL_dC and
+ * aux indexed through perm).  Running all K chunks equals one po_render_backward over the
+ * rays up to the order of the floating-point sums; chunks may run concurrently on several
+ * streams (the gradient accumulation is atomic). */
+po_status po_backward_plan(po_tree* tree, const uint32_t* leaf_span, int64_t n, int32_t K, const int64_t* leaf_bounds,
+                           int32_t* perm, int64_t* chunk_ray_end, int64_t* leaf_end, int64_t* key_quantiles,
+                           po_stream stream);
+po_status po_render_backward_chunk(const po_tree* tree, const float* rays, const int32_t* perm,
+                                   const int64_t* chunk_ray_end, int32_t chunk, const float* dL_dC,
+                                   const double* aux, const po_segments* segments, const po_render_opts* opts,
+                                   float* grad_sigma, float* grad_sh, po_stream stream);
 
 /* Eq. (3) helper: dL_dC[i] = 2 (pred[i] - target[i]) over n*3 floats; if loss != NULL,
  * *loss (device double) = sum (pred - target)^2 (overwritten). */
@@ -148,9 +210,14 @@ po_status po_tree_sgd_step(po_tree* tree, const float* grad_sigma, const float* 
 /* Same update restricted to parameter indices [begin, end) of the index space
  * [0, n_leaves) = sigma~ of leaf i, n_leaves + j = j-th element of grad_sh / sh (leaf-major,
  * [B][3] within a leaf).  Lets the caller update each gradient bucket as soon as its
- * allreduce has landed (a9 overlap).  PO_ERR_INVALID_ARG if the range is outside. */
-po_status po_tree_sgd_step_range(po_tree* tree, const float* grad_sigma, const float* grad_sh, float lr,
-                                 int64_t begin, int64_t end, po_stream stream);
+ * allreduce has landed (a9 overlap).  PO_ERR_INVALID_ARG if the range is outside.
+ * Entries whose gradient is exactly 0 (leaves no ray of the batch composited) are left
+ * untouched (p - lr * 0 = p), so only touched rows are read-modify-written.
+ * flags: PO_SGD_ZERO_GRAD also writes 0 over every consumed gradient entry, so the caller
+ * needs no separate memset before the next backward (the gradients are then non-const). */
+#define PO_SGD_ZERO_GRAD 1
+po_status po_tree_sgd_step_range(po_tree* tree, float* grad_sigma, float* grad_sh, float lr, int64_t begin,
+                                 int64_t end, int32_t flags, po_stream stream);
 
 /* ---- parity / measurement helpers ----------------------------------------------------
  * po_trace: the visited-leaf sequence of each ray up to termination (same traversal as

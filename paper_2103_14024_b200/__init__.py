@@ -25,7 +25,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_destroy", "po_tree_info",
            "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
-           "po_render_backward",
+           "po_render_backward", "po_backward_plan", "po_render_backward_chunk",
            "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
            "po_render_timeline"]
 
@@ -44,6 +44,30 @@ class TreeDesc(ctypes.Structure):
 
 class RenderOpts(ctypes.Structure):
     _fields_ = [("gamma", ctypes.c_float), ("background", ctypes.c_float * 3)]
+
+
+class PoSegments(ctypes.Structure):
+    _fields_ = [("records", ctypes.c_void_p), ("count", ctypes.c_void_p), ("n_rays", ctypes.c_int64),
+                ("max_seg", ctypes.c_int32)]
+
+
+class Segments:
+    """Caller-owned po_segments buffer (include/plenoct.h): records float32 [max_seg][n][8] and
+    count int32 [n] on one device, for the stored-segment pass 2 of a batch of n rays."""
+
+    def __init__(self, n: int, max_seg: int, device=None):
+        import torch
+        self.n, self.max_seg = int(n), int(max_seg)
+        self.records = torch.empty((self.max_seg, self.n, 8), dtype=torch.float32, device=device or "cuda")
+        self.count = torch.empty(self.n, dtype=torch.int32, device=self.records.device)
+
+    def struct(self) -> PoSegments:
+        return PoSegments(self.records.data_ptr() if self.records.numel() else None, self.count.data_ptr(), self.n,
+                          self.max_seg)
+
+
+def _seg(segments):
+    return None if segments is None else ctypes.byref(segments.struct())
 
 
 _lib = None
@@ -66,12 +90,14 @@ def lib():
         L.po_tree_read_leaves.argtypes = [P, P, P]
         L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_host.argtypes = [P, P, I32, I32, I32, P, P, P]
-        L.po_render_rays.argtypes = [P, P, I64, P, P, P, P]
+        L.po_render_rays.argtypes = [P, P, I64, P, P, P, P, P, P]
+        L.po_backward_plan.argtypes = [P, P, I64, I32, P, P, P, P, P, P]
+        L.po_render_backward_chunk.argtypes = [P, P, P, P, I32, P, P, P, P, P, P, P]
         L.po_camera_rays.argtypes = [P, I32, I32, I32, P, I32, P]
-        L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P]
+        L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P, P]
         L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
         L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
-        L.po_tree_sgd_step_range.argtypes = [P, P, P, F, I64, I64, P]
+        L.po_tree_sgd_step_range.argtypes = [P, P, P, F, I64, I64, I32, P]
         L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, P]
         L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_timeline.argtypes = [P, P, I32, I32, I32, P, P, P, P]
@@ -223,7 +249,9 @@ def po_camera_rays(cams, W: int, H: int, stream=None):
 
 
 def po_render_rays(tree: PlenOctree, rays, out=None, aux=None, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
-                   stream=None):
+                   stream=None, leaf_span=None, segments=None):
+    """leaf_span: optional int32 [n][2] tensor (the ABI's uint32 pairs; needs aux) for po_backward_plan;
+    segments: optional Segments(n, max_seg) written for the stored-segment pass 2 (needs aux)."""
     import torch
     rays = _need(rays, torch.float32, (6,))
     n = rays.shape[0]
@@ -232,13 +260,63 @@ def po_render_rays(tree: PlenOctree, rays, out=None, aux=None, gamma: float = 0.
     _need(out, torch.float32, (3,))
     if aux is not None:
         _need(aux, torch.float64, (4,))
+    if leaf_span is not None:
+        _need(leaf_span, torch.int32, (2,))
     o = _opts(gamma, background)
-    _check(lib().po_render_rays(tree.handle, _ptr(rays), n, ctypes.byref(o), _ptr(out), _ptr(aux), _stream(stream)))
+    _check(lib().po_render_rays(tree.handle, _ptr(rays), n, ctypes.byref(o), _ptr(out), _ptr(aux), _ptr(leaf_span),
+                                _seg(segments), _stream(stream)))
     return out
 
 
+def po_backward_plan(tree: PlenOctree, leaf_span, K: int, leaf_bounds=None, perm=None, chunk_ray_end=None,
+                     key_quantiles=None, stream=None):
+    """Chunk plan for overlapping pass 2 with the gradient allreduce (include/plenoct.h).
+    Returns (perm int32 [n], chunk_ray_end int64 [K] on the device, leaf_end list of K ints);
+    key_quantiles (optional int64 [K] device tensor) receives balanced bounds for the next plan."""
+    import torch
+    _need(leaf_span, torch.int32, (2,))
+    n = leaf_span.shape[0]
+    if perm is None:
+        perm = torch.empty(n, dtype=torch.int32, device=leaf_span.device)
+    if chunk_ray_end is None:
+        chunk_ray_end = torch.empty(K, dtype=torch.int64, device=leaf_span.device)
+    _need(perm, torch.int32)
+    _need(chunk_ray_end, torch.int64)
+    if key_quantiles is not None:
+        _need(key_quantiles, torch.int64)
+    bounds = None
+    if leaf_bounds is not None:
+        if len(leaf_bounds) != K:
+            raise ValueError("leaf_bounds needs K entries")
+        bounds = (ctypes.c_int64 * K)(*[int(b) for b in leaf_bounds])
+    leaf_end = (ctypes.c_int64 * K)()
+    _check(lib().po_backward_plan(tree.handle, _ptr(leaf_span), n, int(K), bounds, _ptr(perm), _ptr(chunk_ray_end),
+                                  leaf_end, _ptr(key_quantiles), _stream(stream)))
+    return perm, chunk_ray_end, list(leaf_end)
+
+
+def po_render_backward_chunk(tree: PlenOctree, rays, perm, chunk_ray_end, chunk: int, dL_dC, grad_sigma, grad_sh,
+                             aux=None, gamma: float = 0.0, background=(1.0, 1.0, 1.0), stream=None, segments=None):
+    """po_render_backward over chunk `chunk` of a po_backward_plan (accumulates, +=)."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    _need(perm, torch.int32)
+    _need(chunk_ray_end, torch.int64)
+    if not 0 <= chunk < chunk_ray_end.shape[0]:
+        raise ValueError("chunk outside the plan")
+    _need(dL_dC, torch.float32, (3,))
+    _need(grad_sigma, torch.float32)
+    _need(grad_sh, torch.float32, (tree.B, 3))
+    if aux is not None:
+        _need(aux, torch.float64, (4,))
+    o = _opts(gamma, background)
+    _check(lib().po_render_backward_chunk(tree.handle, _ptr(rays), _ptr(perm), _ptr(chunk_ray_end), int(chunk),
+                                          _ptr(dL_dC), _ptr(aux), _seg(segments), ctypes.byref(o), _ptr(grad_sigma),
+                                          _ptr(grad_sh), _stream(stream)))
+
+
 def po_render_backward(tree: PlenOctree, rays, dL_dC, grad_sigma, grad_sh, aux=None, gamma: float = 0.0,
-                       background=(1.0, 1.0, 1.0), stream=None):
+                       background=(1.0, 1.0, 1.0), stream=None, segments=None):
     """Accumulates (+=) dL/dsigma~ into grad_sigma [n_leaves] and dL/dk into grad_sh [n_leaves][B][3]."""
     import torch
     rays = _need(rays, torch.float32, (6,))
@@ -248,8 +326,8 @@ def po_render_backward(tree: PlenOctree, rays, dL_dC, grad_sigma, grad_sh, aux=N
     if aux is not None:
         _need(aux, torch.float64, (4,))
     o = _opts(gamma, background)
-    _check(lib().po_render_backward(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux), ctypes.byref(o),
-                                    _ptr(grad_sigma), _ptr(grad_sh), _stream(stream)))
+    _check(lib().po_render_backward(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux), _seg(segments),
+                                    ctypes.byref(o), _ptr(grad_sigma), _ptr(grad_sh), _stream(stream)))
 
 
 def po_l2_loss_grad(pred, target, dL_dC=None, loss=None, stream=None):
@@ -269,9 +347,13 @@ def po_tree_sgd_step(tree: PlenOctree, grad_sigma, grad_sh, lr: float, stream=No
     _check(lib().po_tree_sgd_step(tree.handle, _ptr(grad_sigma), _ptr(grad_sh), float(lr), _stream(stream)))
 
 
-def po_tree_sgd_step_range(tree: PlenOctree, grad_sigma, grad_sh, lr: float, begin: int, end: int, stream=None):
+PO_SGD_ZERO_GRAD = 1
+
+
+def po_tree_sgd_step_range(tree: PlenOctree, grad_sigma, grad_sh, lr: float, begin: int, end: int, stream=None,
+                           zero_grad: bool = False):
     _check(lib().po_tree_sgd_step_range(tree.handle, _ptr(grad_sigma), _ptr(grad_sh), float(lr), int(begin), int(end),
-                                        _stream(stream)))
+                                        PO_SGD_ZERO_GRAD if zero_grad else 0, _stream(stream)))
 
 
 def po_trace(tree: PlenOctree, rays, max_leaves: int = 64, gamma: float = 0.01, with_nodes: bool = True,

@@ -1,5 +1,6 @@
 // C-ABI layer of libplenoct (include/plenoct.h): argument validation, tree upload (a0),
 // device selection and kernel launches.  No compute happens here; there is no CPU path.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -49,6 +50,10 @@ struct po_tree {
     std::atomic<uint32_t> work_rr{0};
     int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
     unsigned* work_of(int slot) { return d_work + 2 * slot; }
+    // po_backward_plan scratch (sort keys/values + CUB temp), grown on demand
+    void* d_plan = nullptr;
+    size_t plan_cap = 0;
+    std::mutex plan_mu;
 };
 
 namespace {
@@ -443,6 +448,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_macro) cudaFree(t->d_macro);
     if (t->d_child_b) cudaFree(t->d_child_b);
     if (t->d_brick) cudaFree(t->d_brick);
+    if (t->d_plan) cudaFree(t->d_plan);
     t->d_child = nullptr;
     delete t;
     return PO_OK;
@@ -583,34 +589,140 @@ po_status po_camera_rays(const po_camera* cams, int32_t n_cams, int32_t W, int32
     return launched(po::launch_camera_rays(cams, n_cams, W, H, rays, (cudaStream_t)stream), "po_camera_rays");
 }
 
+// po_segments -> launcher struct; n_expect < 0 skips the batch-size check (chunked backward)
+static po_status check_segments(const po_segments* sg, int64_t n_expect, const void* aux, po::Segments* out) {
+    *out = po::Segments{nullptr, nullptr, 0, 0};
+    if (!sg) return PO_OK;
+    if (!aux) return fail(PO_ERR_INVALID_ARG, "segments need aux (pass-1 / pass-2 pairing)");
+    if ((!sg->records && sg->max_seg > 0) || !sg->count) return fail(PO_ERR_INVALID_ARG, "segments: NULL records / count");
+    if (sg->max_seg < 0) return fail(PO_ERR_INVALID_ARG, "segments: max_seg < 0");
+    if (((uintptr_t)sg->records & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "segments: records not 16-byte aligned");
+    if (sg->n_rays < 0 || (n_expect >= 0 && sg->n_rays != n_expect))
+        return fail(PO_ERR_INVALID_ARG, "segments: n_rays %lld does not match the batch", (long long)sg->n_rays);
+    *out = po::Segments{sg->records, sg->count, sg->n_rays, sg->max_seg};
+    return PO_OK;
+}
+
 po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, float* out_rgb,
-                         double* aux, po_stream stream) {
+                         double* aux, uint32_t* leaf_span, const po_segments* segments, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
     po::RenderOpts o;
     if (po_status s = check_opts(opts, &o)) return s;
     if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (leaf_span && !aux) return fail(PO_ERR_INVALID_ARG, "leaf_span needs aux (pass-1 mode)");
+    if (leaf_span && ((uintptr_t)leaf_span & 7u) != 0) return fail(PO_ERR_INVALID_ARG, "leaf_span not 8-byte aligned");
+    po::Segments sg;
+    if (po_status s = check_segments(segments, n, aux, &sg)) return s;
     if (n == 0) return PO_OK;
     if (!rays || !out_rgb) return fail(PO_ERR_INVALID_ARG, "rays / out_rgb NULL");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_render_rays(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, o,
-                                           out_rgb, aux, (cudaStream_t)stream),
+                                           out_rgb, aux, leaf_span, sg, (cudaStream_t)stream),
                     "po_render_rays");
 }
 
+po_status po_backward_plan(po_tree* t, const uint32_t* leaf_span, int64_t n, int32_t K, const int64_t* leaf_bounds,
+                           int32_t* perm, int64_t* chunk_ray_end, int64_t* leaf_end, int64_t* key_quantiles,
+                           po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(PO_ERR_INVALID_ARG, "n outside [0, 2^31)");
+    if (K < 1 || K > po::kMaxPlanChunks) return fail(PO_ERR_INVALID_ARG, "K outside [1, %d]", po::kMaxPlanChunks);
+    if (!chunk_ray_end || (n > 0 && (!leaf_span || !perm))) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    if (t->n_leaves >= (int64_t)0xFFFFFFFFu) return fail(PO_ERR_UNSUPPORTED, "n_leaves >= 2^32");
+    po::PlanBounds pb{};
+    pb.K = K;
+    for (int32_t j = 0; j < K; ++j) {
+        pb.b[j] = leaf_bounds ? leaf_bounds[j] : t->n_leaves * (int64_t)(j + 1) / K;
+        if (pb.b[j] < (j ? pb.b[j - 1] : 0) || pb.b[j] > t->n_leaves)
+            return fail(PO_ERR_INVALID_ARG, "leaf_bounds not non-decreasing in [0, n_leaves]");
+    }
+    if (pb.b[K - 1] != t->n_leaves) return fail(PO_ERR_INVALID_ARG, "leaf_bounds[K-1] != n_leaves");
+    if (leaf_end)
+        for (int32_t j = 0; j < K; ++j) leaf_end[j] = pb.b[j];
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        cudaError_t e = cudaMemsetAsync(chunk_ray_end, 0, sizeof(int64_t) * K, s);
+        if (e == cudaSuccess && key_quantiles) {
+            std::vector<int64_t> q((size_t)K, t->n_leaves);
+            e = cudaMemcpyAsync(key_quantiles, q.data(), sizeof(int64_t) * K, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // q is a stack buffer
+        }
+        return e == cudaSuccess ? PO_OK : cuda_status(e, "po_backward_plan (n = 0)");
+    }
+    // keys = lowest sigma~>0 leaf per ray (n_leaves when the ray has none), sorted stably
+    // with the ray index as value: rays keep their relative order inside equal keys
+    int end_bit = 1;
+    while (end_bit < 32 && ((uint64_t)1 << end_bit) <= (uint64_t)t->n_leaves) ++end_bit;
+    size_t cub_bytes = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)n, 0, end_bit, s);
+    if (e != cudaSuccess) return cuda_status(e, "cub sizing");
+    const size_t arr = ((size_t)n * 4 + 255) / 256 * 256;
+    const size_t need = 3 * arr + cub_bytes;
+    std::lock_guard<std::mutex> lk(t->plan_mu);
+    if (t->plan_cap < need) {
+        if (t->d_plan) cudaFree(t->d_plan);
+        t->d_plan = nullptr;
+        t->plan_cap = 0;
+        e = cudaMalloc(&t->d_plan, need);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(plan scratch)");
+        t->plan_cap = need;
+    }
+    char* base = static_cast<char*>(t->d_plan);
+    uint32_t* keys_in = reinterpret_cast<uint32_t*>(base);
+    uint32_t* keys_out = reinterpret_cast<uint32_t*>(base + arr);
+    int32_t* idx_in = reinterpret_cast<int32_t*>(base + 2 * arr);
+    void* tmp = base + 3 * arr;
+    if ((e = po::launch_plan_keys(leaf_span, n, (uint32_t)t->n_leaves, keys_in, idx_in, s)) != cudaSuccess)
+        return cuda_status(e, "plan keys");
+    g_launches.fetch_add(1);
+    e = cub::DeviceRadixSort::SortPairs(tmp, cub_bytes, keys_in, keys_out, idx_in, perm, (int)n, 0, end_bit, s);
+    if (e != cudaSuccess) return cuda_status(e, "cub sort");
+    return launched(po::launch_plan_ends(keys_out, n, t->n_leaves, pb, chunk_ray_end, key_quantiles, s),
+                    "po_backward_plan");
+}
+
+po_status po_render_backward_chunk(const po_tree* t, const float* rays, const int32_t* perm,
+                                   const int64_t* chunk_ray_end, int32_t chunk, const float* dL_dC, const double* aux,
+                                   const po_segments* segments, const po_render_opts* opts, float* grad_sigma,
+                                   float* grad_sh, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    po::Segments sg;
+    if (po_status s = check_segments(segments, -1, aux, &sg)) return s;
+    if (chunk < 0) return fail(PO_ERR_INVALID_ARG, "chunk < 0");
+    if (!rays || !perm || !chunk_ray_end || !dL_dC || !grad_sigma || !grad_sh)
+        return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    po_tree* mt = const_cast<po_tree*>(t);   // work counters only
+    return launched(po::launch_backward_chunk(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, perm,
+                                              chunk_ray_end, chunk, dL_dC, aux, sg, o, grad_sigma, grad_sh,
+                                              mt->work_of(mt->next_slot()), (cudaStream_t)stream),
+                    "po_render_backward_chunk");
+}
+
 po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, const float* dL_dC, const double* aux,
-                             const po_render_opts* opts, float* grad_sigma, float* grad_sh, po_stream stream) {
+                             const po_segments* segments, const po_render_opts* opts, float* grad_sigma,
+                             float* grad_sh, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
     po::RenderOpts o;
     if (po_status s = check_opts(opts, &o)) return s;
     if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    po::Segments sg;
+    if (po_status s = check_segments(segments, n, aux, &sg)) return s;
     if (n == 0) return PO_OK;
     if (!rays || !dL_dC || !grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
-                                        o, grad_sigma, grad_sh, (cudaStream_t)stream),
+                                        sg, o, grad_sigma, grad_sh, (cudaStream_t)stream),
                     "po_render_backward");
 }
 
@@ -623,8 +735,8 @@ po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, flo
     return launched(po::launch_l2_loss(pred, target, n * 3, dL_dC, loss, (cudaStream_t)stream), "po_l2_loss_grad");
 }
 
-po_status po_tree_sgd_step_range(po_tree* t, const float* grad_sigma, const float* grad_sh, float lr, int64_t begin,
-                                 int64_t end, po_stream stream) {
+po_status po_tree_sgd_step_range(po_tree* t, float* grad_sigma, float* grad_sh, float lr, int64_t begin, int64_t end,
+                                 int32_t flags, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
     if (t->desc.payload != PO_F32) return fail(PO_ERR_UNSUPPORTED, "SGD needs an fp32 payload (P:973 trains in fp32)");
     if (!std::isfinite(lr)) return fail(PO_ERR_INVALID_ARG, "lr not finite");
@@ -634,16 +746,20 @@ po_status po_tree_sgd_step_range(po_tree* t, const float* grad_sigma, const floa
                     (long long)total);
     if (end == begin) return PO_OK;
     if (!grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL gradient");
+    if (flags & ~PO_SGD_ZERO_GRAD) return fail(PO_ERR_INVALID_ARG, "unknown flags %d", flags);
+    if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_sgd(t->d_sigma, static_cast<float*>(t->d_sh), t->sh_row, t->ne, t->n_leaves, grad_sigma,
-                                   grad_sh, lr, begin, end, (cudaStream_t)stream),
+                                   grad_sh, lr, begin, end, (flags & PO_SGD_ZERO_GRAD) != 0, (cudaStream_t)stream),
                     "po_tree_sgd_step");
 }
 
 po_status po_tree_sgd_step(po_tree* t, const float* grad_sigma, const float* grad_sh, float lr, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
-    return po_tree_sgd_step_range(t, grad_sigma, grad_sh, lr, 0, t->n_leaves * (int64_t)(t->ne + 1), stream);
+    // flags = 0: the gradients are only read
+    return po_tree_sgd_step_range(t, const_cast<float*>(grad_sigma), const_cast<float*>(grad_sh), lr, 0,
+                                  t->n_leaves * (int64_t)(t->ne + 1), 0, stream);
 }
 
 po_status po_trace(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, int32_t max_leaves,

@@ -160,6 +160,17 @@ struct FwdVisitorSm {
     }
 };
 
+// Stored pass-1 segments (po_segments): record k of ray i = two float4 at (k n + i) * 2:
+// (leaf index bits, delta, w, T_{i+1}), (c_r, c_g, c_b, 0) -- every value pass 2 needs, so it
+// replays the segments instead of re-traversing the tree.  count[i] = number of sigma~ > 0
+// segments, max_seg + 1 when they did not fit (pass 2 then re-traverses that ray).
+struct SegOut {
+    float4* __restrict__ rec;
+    int32_t* __restrict__ count;
+    int64_t n;
+    int32_t max_seg;
+};
+
 // Forward with the colour sum accumulated in double (pass 1 of the backward).
 template <int DEG, bool F16>
 struct TotalVisitor {
@@ -167,7 +178,12 @@ struct TotalVisitor {
     float Y[ShDim<DEG>::B];
     float T, gamma;
     double C[3];
-    __device__ TotalVisitor(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g) {
+    uint32_t lo, hi;   // [lo, hi]: index span of the sigma~ > 0 leaves composited (po_backward_plan)
+    float4* __restrict__ seg;   // this ray's first record (SegOut) or null
+    int64_t seg_stride;         // 2 n float4 between consecutive records of a ray
+    int32_t nseg, max_seg;      // max_seg < 0: no segment bookkeeping
+    __device__ TotalVisitor(const DevTree& t, const float d[3], float g)
+        : tr(t), T(1.f), gamma(g), lo(0xFFFFFFFFu), hi(0u), seg(nullptr), seg_stride(0), nseg(0), max_seg(-1) {
         sh_basis<DEG>(d, t.odd_sign, Y);
         C[0] = C[1] = C[2] = 0.0;
     }
@@ -177,9 +193,24 @@ struct TotalVisitor {
         float z[3];
         sh_dot<DEG, F16>(tr, idx, Y, z);   // row loads in flight together with sigma
         if (!(st > 0.f)) return true;
-        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+        lo = min(lo, idx);
+        hi = max(hi, idx);
+        const float delta = __fsub_rn(t1, t0);
+        const Absorb a = absorb(T, st, delta);
+        float c[3];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) C[ch] += (double)a.w * (double)sigmoidf_(z[ch]);
+        for (int ch = 0; ch < 3; ++ch) {
+            c[ch] = sigmoidf_(z[ch]);
+            C[ch] += (double)a.w * (double)c[ch];
+        }
+        if (max_seg >= 0) {
+            if (nseg < max_seg) {
+                float4* r = seg + (int64_t)nseg * seg_stride;
+                r[0] = make_float4(__uint_as_float(idx), delta, a.w, a.Tn);
+                r[1] = make_float4(c[0], c[1], c[2], 0.f);
+            }
+            nseg = min(nseg + 1, max_seg + 1);
+        }
         T = a.Tn;
         return !(T < gamma);
     }
@@ -210,19 +241,27 @@ struct GradVisitor {
         if (!(st > 0.f)) return true;   // ReLU gate: w = 0 and dsigma = 0
         const float delta = __fsub_rn(t1, t0);
         const Absorb a = absorb(T, st, delta);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) c[ch] = sigmoidf_(z[ch]);
+        seg(idx, delta, a.w, a.Tn, c);
+        T = a.Tn;
+        return !(T < gamma);
+    }
+    // gradient of one sigma~ > 0 segment from its forward values (w_i, T_{i+1}, c_i): used by
+    // the re-traversal above and by the stored-segment replay (identical arithmetic)
+    __device__ __forceinline__ void seg(uint32_t idx, float delta, float w, float Tn, const float c[3]) {
         double acc = 0.0;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            c[ch] = sigmoidf_(z[ch]);
-            P[ch] += (double)a.w * (double)c[ch];
-            acc += (double)g[ch] * ((double)c[ch] * (double)a.Tn - (Ctot[ch] - P[ch]));
+            P[ch] += (double)w * (double)c[ch];
+            acc += (double)g[ch] * ((double)c[ch] * (double)Tn - (Ctot[ch] - P[ch]));
         }
         atomicAdd(grad_sigma + idx, (float)((double)delta * acc));
         constexpr int B = ShDim<DEG>::B;
         constexpr int NE = 3 * B;
         float gz[3];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) gz[ch] = g[ch] * a.w * c[ch] * (1.f - c[ch]);
+        for (int ch = 0; ch < 3; ++ch) gz[ch] = g[ch] * w * c[ch] * (1.f - c[ch]);
         float* row = grad_sh + (size_t)idx * NE;
         if constexpr (NE % 4 == 0) {
 #pragma unroll
@@ -239,8 +278,6 @@ struct GradVisitor {
 #pragma unroll
             for (int el = 0; el < NE; ++el) atomicAdd(row + el, gz[el % 3] * Y[el / 3]);
         }
-        T = a.Tn;
-        return !(T < gamma);
     }
 };
 
@@ -466,7 +503,8 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
 
 template <int DEG, bool F16>
 __global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
-                                                     RenderOpts opt, float* __restrict__ out, double* __restrict__ aux) {
+                                                     RenderOpts opt, float* __restrict__ out, double* __restrict__ aux,
+                                                     uint32_t* __restrict__ span, SegOut so) {
     PO_DECLARE_STACK(stk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -491,10 +529,20 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float*
     } else {
         double C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
         float T = 1.f;
+        uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+        int32_t nseg = 0;
         if (hit) {
             TotalVisitor<DEG, F16> v(tr, r.d, opt.gamma);
+            if (so.count != nullptr) {
+                v.seg = so.rec != nullptr ? so.rec + 2 * i : nullptr;
+                v.seg_stride = 2 * so.n;
+                v.max_seg = so.max_seg;
+            }
             traverse(tr, r, v, stk);
+            nseg = v.nseg;
             T = v.T;
+            lo = v.lo;
+            hi = v.hi;
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) C[ch] = v.C[ch] + (double)v.T * (double)opt.bg[ch];
         }
@@ -504,17 +552,29 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float*
             aux[i * 4 + ch] = C[ch];
         }
         aux[i * 4 + 3] = (double)T;
+        if (span != nullptr) reinterpret_cast<uint2*>(span)[i] = make_uint2(lo, hi);
+        if (so.count != nullptr) so.count[i] = nseg;
     }
 }
 
-template <int DEG, bool F16>
-__global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __restrict__ rays, int64_t n,
-                                                  const float* __restrict__ dL_dC, const double* __restrict__ aux,
-                                                  RenderOpts opt, float* __restrict__ grad_sigma,
-                                                  float* __restrict__ grad_sh) {
-    PO_DECLARE_STACK(stk);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+struct SegIn {
+    const float4* __restrict__ rec;
+    const int32_t* __restrict__ count;
+    int64_t n;
+    int32_t max_seg;
+};
+
+// One training ray of pass 2 (a7 + a8): total from aux (or its own pass 1), then the
+// gradient traversal.  Shared by k_backward (one thread per ray) and k_backward_chunk.
+// kSkipReplay: rays whose segments are stored return at once (k_backward_replay has them)
+template <int DEG, bool F16, bool kSkipReplay = false>
+__device__ __forceinline__ void backward_ray(const DevTree& tr, const float* __restrict__ rays, int64_t i,
+                                             const float* __restrict__ dL_dC, const double* __restrict__ aux,
+                                             const SegIn& si, const RenderOpts& opt, float* __restrict__ grad_sigma,
+                                             float* __restrict__ grad_sh, const SmemStack& stk) {
+    if constexpr (kSkipReplay) {
+        if (__ldg(si.count + i) <= si.max_seg) return;
+    }
     float o[3], d[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -527,6 +587,20 @@ __global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) gv.g[ch] = __ldg(dL_dC + i * 3 + ch);
     if (gv.g[0] == 0.f && gv.g[1] == 0.f && gv.g[2] == 0.f) return;
+    if (aux != nullptr && si.count != nullptr) {
+        const int32_t ns = __ldg(si.count + i);
+        if (ns <= si.max_seg) {   // replay the stored segments: no traversal, no SH rows
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = aux[i * 4 + ch];
+            const float4* rec = si.rec + 2 * i;   // unused when ns == 0 (max_seg may be 0)
+            for (int32_t k = 0; k < ns; ++k, rec += 2 * si.n) {
+                const float4 a = __ldg(rec), b = __ldg(rec + 1);
+                const float c[3] = {b.x, b.y, b.z};
+                gv.seg(__float_as_uint(a.x), a.y, a.z, a.w, c);
+            }
+            return;
+        }
+    }
     if (aux != nullptr) {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = aux[i * 4 + ch];
@@ -537,6 +611,169 @@ __global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __
         for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = tv.C[ch] + (double)tv.T * (double)opt.bg[ch];
     }
     traverse(tr, r, gv, stk);
+}
+
+template <int DEG, bool F16, bool kSkipReplay>
+__global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                  const float* __restrict__ dL_dC, const double* __restrict__ aux,
+                                                  SegIn si, RenderOpts opt, float* __restrict__ grad_sigma,
+                                                  float* __restrict__ grad_sh) {
+    PO_DECLARE_STACK(stk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    backward_ray<DEG, F16, kSkipReplay>(tr, rays, i, dL_dC, aux, si, opt, grad_sigma, grad_sh, stk);
+}
+
+// Stored-segment pass 2, one WARP per ray: lane l takes segments l, l+32, ... of the ray, so
+// the record loads of a ray are in flight together instead of forming a per-thread chain
+// (the one-thread-per-ray replay was load-latency bound: 1.27 ms on c4, 70 % long-scoreboard
+// stalls).  The prefix P_i = sum_{k<=i} w_k c_k is an inclusive warp scan in double carried
+// across 32-segment rounds (same sum as the sequential pass up to double rounding order);
+// then every lane applies GradVisitor::seg's formula to its own segment.  Rays whose segments
+// overflowed (count > max_seg) are left to k_backward<..., true>.
+template <int DEG>
+__global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                         const float* __restrict__ dL_dC,
+                                                         const double* __restrict__ aux, SegIn si,
+                                                         float* __restrict__ grad_sigma,
+                                                         float* __restrict__ grad_sh) {
+    constexpr int B = ShDim<DEG>::B;
+    constexpr int NE = 3 * B;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const int32_t ns = __ldg(si.count + i);
+    if (ns == 0 || ns > si.max_seg) return;
+    float g[3], dir[3], d[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) g[ch] = __ldg(dL_dC + i * 3 + ch);
+    if (g[0] == 0.f && g[1] == 0.f && g[2] == 0.f) return;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dir[k] = __ldg(rays + i * 6 + 3 + k);
+    if (!unit_direction(dir, d)) return;
+    float Y[B];
+    sh_basis<DEG>(d, tr.odd_sign, Y);
+    double Ctot[3], carry[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) Ctot[ch] = aux[i * 4 + ch];
+    for (int32_t base = 0; base < ns; base += 32) {
+        const int32_t k = base + lane;
+        const bool act = k < ns;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (act) {
+            const float4* rec = si.rec + 2 * ((int64_t)k * si.n + i);
+            a = __ldg(rec);
+            b = __ldg(rec + 1);
+        }
+        const float c[3] = {b.x, b.y, b.z};
+        double P[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            double v = (double)a.z * (double)c[ch];   // w_k c_k (0 for inactive lanes)
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double u = __shfl_up_sync(0xFFFFFFFFu, v, off);
+                if (lane >= off) v += u;
+            }
+            P[ch] = carry[ch] + v;
+            carry[ch] = __shfl_sync(0xFFFFFFFFu, P[ch], 31);
+        }
+        if (!act) continue;
+        const uint32_t idx = __float_as_uint(a.x);
+        const float delta = a.y, w = a.z, Tn = a.w;
+        double acc = 0.0;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) acc += (double)g[ch] * ((double)c[ch] * (double)Tn - (Ctot[ch] - P[ch]));
+        atomicAdd(grad_sigma + idx, (float)((double)delta * acc));
+        float gz[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gz[ch] = g[ch] * w * c[ch] * (1.f - c[ch]);
+        float* row = grad_sh + (size_t)idx * NE;
+        if constexpr (NE % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < NE / 4; ++j) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3];
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * j), "f"(v[0]),
+                             "f"(v[1]), "f"(v[2]), "f"(v[3])
+                             : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int el = 0; el < NE; ++el) atomicAdd(row + el, gz[el % 3] * Y[el / 3]);
+        }
+    }
+}
+
+// Pass 2 over one chunk of a po_backward_plan: rays perm[chunk_end[c-1] .. chunk_end[c]).
+// The bounds live on the device (no host sync between the plan and the chunks), so the grid
+// is persistent and warps claim 32-ray batches from a global counter (work[0]); no warp waits
+// for a slower one (CTA-wide 256-ray claims measured 5 % slower at K = 2 and 4); the last CTA
+// resets the counters (work[1] = finished CTAs) for the next launch on the stream.
+template <int DEG, bool F16>
+__global__ void __launch_bounds__(256, 2) k_backward_chunk(DevTree tr, const float* __restrict__ rays,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int64_t* __restrict__ chunk_end, int chunk,
+                                                        const float* __restrict__ dL_dC,
+                                                        const double* __restrict__ aux, SegIn si, RenderOpts opt,
+                                                        float* __restrict__ grad_sigma, float* __restrict__ grad_sh,
+                                                        unsigned* __restrict__ work) {
+    PO_DECLARE_STACK(stk);
+    const int64_t b = chunk > 0 ? chunk_end[chunk - 1] : 0, e = chunk_end[chunk];
+    const int64_t nb = (e - b + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned k = 0;
+        if (lane == 0) k = atomicAdd(work, 1u);
+        k = __shfl_sync(0xFFFFFFFFu, k, 0);
+        if ((int64_t)k >= nb) break;
+        const int64_t j = b + ((int64_t)k << 5) + lane;
+        if (j < e)
+            backward_ray<DEG, F16>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, opt, grad_sigma, grad_sh, stk);
+        __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            atomicExch(work, 0u);
+            atomicExch(work + 1, 0u);
+        }
+    }
+}
+
+// po_backward_plan helpers: sort keys = first sigma~>0 leaf of each ray (n_leaves if none)
+__global__ void __launch_bounds__(256) k_plan_keys(const uint32_t* __restrict__ span, int64_t n, uint32_t n_leaves,
+                                                   uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = min(__ldg(span + 2 * i), n_leaves);
+    idx[i] = (int32_t)i;
+}
+
+// chunk_end[j] = #rays whose key < b_j (bounds from the host); quant[j] (optional) = the key
+// that splits the rays with a sigma>0 leaf into K equal parts -- balanced bounds for the next
+// plan (the caller feeds them back; any monotone bounds keep the finality invariant)
+__global__ void k_plan_ends(const uint32_t* __restrict__ sorted_keys, int64_t n, int64_t n_leaves, PlanBounds bounds,
+                            int64_t* __restrict__ chunk_end, int64_t* __restrict__ quant) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= bounds.K) return;
+    auto lower_bound = [&](int64_t v) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)sorted_keys[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    chunk_end[j] = lower_bound(bounds.b[j]);
+    if (quant != nullptr) {
+        const int64_t n_hit = lower_bound(n_leaves);
+        const int64_t pos = n_hit * (int64_t)(j + 1) / bounds.K;
+        quant[j] = (j == bounds.K - 1 || pos >= n_hit) ? n_leaves : (int64_t)sorted_keys[pos];
+    }
 }
 
 __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restrict__ rays, int64_t n, float gamma,
@@ -614,20 +851,62 @@ __global__ void __launch_bounds__(256) k_l2_loss(const float* __restrict__ pred,
     }
 }
 
+// a9 SGD: p -= lr g over parameter indices [begin, end) ([0, n_leaves) sigma~, then
+// the SH elements leaf-major).  Entries with g == 0 are skipped (p - lr 0 = p exactly), so
+// leaves no ray touched cost one gradient read; zero_grad writes 0 over consumed entries
+// (replaces the caller's memset).  The SH part moves float4 quads when rows are multiples of 4
+// (16-B aligned in both the gradient and the padded leaf rows).
 __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* __restrict__ sh, int32_t sh_row,
-                                             int32_t ne, int64_t n_leaves, const float* __restrict__ grad_sigma,
-                                             const float* __restrict__ grad_sh, float lr, int64_t begin,
-                                             int64_t end) {
-    for (int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < n_leaves) {
-            sigma[i] -= lr * grad_sigma[i];
-        } else {
-            const int64_t j = i - n_leaves;
-            const int64_t leaf = j / ne;
-            const int64_t el = j - leaf * ne;
-            sh[leaf * sh_row + el] -= lr * grad_sh[j];
+                                             int32_t ne, int64_t n_leaves, float* __restrict__ grad_sigma,
+                                             float* __restrict__ grad_sh, float lr, int64_t begin, int64_t end,
+                                             bool zero_grad) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = begin + tid; i < min(end, n_leaves); i += nth) {
+        const float g = grad_sigma[i];
+        if (g != 0.f) {
+            sigma[i] -= lr * g;
+            if (zero_grad) grad_sigma[i] = 0.f;
         }
+    }
+    if (end <= n_leaves) return;
+    const int64_t hb = max(begin, n_leaves) - n_leaves, he = end - n_leaves;   // SH element range
+    auto scalar = [&](int64_t j) {
+        const float g = grad_sh[j];
+        if (g != 0.f) {
+            const int64_t leaf = j / ne;
+            sh[leaf * sh_row + (j - leaf * ne)] -= lr * g;
+            if (zero_grad) grad_sh[j] = 0.f;
+        }
+    };
+    if ((ne & 3) != 0) {
+        for (int64_t j = hb + tid; j < he; j += nth) scalar(j);
+        return;
+    }
+    const int64_t qb = (hb + 3) >> 2, qe = he >> 2;   // whole quads inside the range
+    if (qb >= qe) {
+        for (int64_t j = hb + tid; j < he; j += nth) scalar(j);
+        return;
+    }
+    if (tid < 4) {   // ragged head / tail of the range
+        const int64_t j0 = hb + tid, j1 = (qe << 2) + tid;
+        if (j0 < (qb << 2)) scalar(j0);
+        if (j1 < he) scalar(j1);
+    }
+    const uint32_t qpr = (uint32_t)(ne >> 2);   // quads per leaf row
+    float4* __restrict__ g4 = reinterpret_cast<float4*>(grad_sh);
+    for (int64_t q = qb + tid; q < qe; q += nth) {
+        const float4 g = g4[q];
+        if (g.x == 0.f && g.y == 0.f && g.z == 0.f && g.w == 0.f) continue;
+        const int64_t leaf = (q < ((int64_t)1 << 32)) ? (int64_t)((uint32_t)q / qpr) : q / qpr;
+        float4* p = reinterpret_cast<float4*>(sh + leaf * sh_row) + (q - leaf * qpr);
+        float4 v = *p;
+        v.x -= lr * g.x;
+        v.y -= lr * g.y;
+        v.z -= lr * g.z;
+        v.w -= lr * g.w;
+        *p = v;
+        if (zero_grad) g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -766,22 +1045,61 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
 }
 
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
-                               const RenderOpts& opt, float* out, double* aux, cudaStream_t s) {
+                               const RenderOpts& opt, float* out, double* aux, uint32_t* span, const Segments& sg,
+                               cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    const SegOut so{static_cast<float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
     PO_DISPATCH(deg, f16, {
         carveout_once(k_render_rays<DEG, F16>);
-        k_render_rays<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out, aux);
+        k_render_rays<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out, aux, span, so);
     });
     return cudaGetLastError();
 }
 
-cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
-                            const double* aux, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
-                            cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
+cudaError_t launch_backward_chunk(const DevTree& tr, int deg, bool f16, const float* rays, const int32_t* perm,
+                                  const int64_t* chunk_end, int chunk, const float* dL_dC, const double* aux,
+                                  const Segments& sg, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
+                                  unsigned* work, cudaStream_t s) {
+    const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
     PO_DISPATCH(deg, f16, {
-        carveout_once(k_backward<DEG, F16>);
-        k_backward<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, opt, grad_sigma, grad_sh);
+        static const int grid = persistent_grid(k_backward_chunk<DEG, F16>, 1 << 30, 0);
+        k_backward_chunk<DEG, F16><<<grid, 256, 0, s>>>(tr, rays, perm, chunk_end, chunk, dL_dC, aux, si, opt,
+                                                        grad_sigma, grad_sh, work);
+    });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan_keys(const uint32_t* span, int64_t n, uint32_t n_leaves, uint32_t* keys, int32_t* idx,
+                             cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_plan_keys<<<grid1d(n, 256), 256, 0, s>>>(span, n, n_leaves, keys, idx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan_ends(const uint32_t* sorted_keys, int64_t n, int64_t n_leaves, const PlanBounds& b,
+                             int64_t* chunk_end, int64_t* quant, cudaStream_t s) {
+    k_plan_ends<<<1, 64, 0, s>>>(sorted_keys, n, n_leaves, b, chunk_end, quant);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
+                            const double* aux, const Segments& sg, const RenderOpts& opt, float* grad_sigma,
+                            float* grad_sh, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+    const bool replay = aux != nullptr && sg.count != nullptr;
+    PO_DISPATCH(deg, f16, {
+        if (replay) {   // stored segments first, then the overflow rays by re-traversal
+            carveout_once(k_backward_replay<DEG>);
+            k_backward_replay<DEG><<<grid1d(n, 8), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, grad_sigma, grad_sh);
+            carveout_once(k_backward<DEG, F16, true>);
+            k_backward<DEG, F16, true><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, opt, grad_sigma,
+                                                                      grad_sh);
+        } else {
+            carveout_once(k_backward<DEG, F16, false>);
+            k_backward<DEG, F16, false><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, opt, grad_sigma,
+                                                                       grad_sh);
+        }
     });
     return cudaGetLastError();
 }
@@ -815,12 +1133,12 @@ cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, f
     return cudaGetLastError();
 }
 
-cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, const float* grad_sigma,
-                       const float* grad_sh, float lr, int64_t begin, int64_t end, cudaStream_t s) {
+cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, float* grad_sigma,
+                       float* grad_sh, float lr, int64_t begin, int64_t end, bool zero_grad, cudaStream_t s) {
     if (end <= begin) return cudaSuccess;
-    unsigned g = grid1d(end - begin, 256);
-    if (g > 148 * 32) g = 148 * 32;
-    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr, begin, end);
+    unsigned g = grid1d(end - begin, 256 * 4);
+    if (g > 148 * 16) g = 148 * 16;
+    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr, begin, end, zero_grad);
     return cudaGetLastError();
 }
 

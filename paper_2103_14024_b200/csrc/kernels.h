@@ -22,18 +22,39 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
                           const RenderOpts& opt, float* out, unsigned* work, const unsigned* order,
                           unsigned long long* timeline, cudaStream_t s);
 cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, float* rays, cudaStream_t s);
+// stored pass-1 segments (po_segments): rec = float[max_seg][n][8] or null
+struct Segments {
+    void* rec;
+    int32_t* count;
+    int64_t n;
+    int32_t max_seg;
+};
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
-                               const RenderOpts& opt, float* out, double* aux, cudaStream_t s);
+                               const RenderOpts& opt, float* out, double* aux, uint32_t* span, const Segments& sg,
+                               cudaStream_t s);
+cudaError_t launch_backward_chunk(const DevTree& tr, int deg, bool f16, const float* rays, const int32_t* perm,
+                                  const int64_t* chunk_end, int chunk, const float* dL_dC, const double* aux,
+                                  const Segments& sg, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
+                                  unsigned* work, cudaStream_t s);
+cudaError_t launch_plan_keys(const uint32_t* span, int64_t n, uint32_t n_leaves, uint32_t* keys, int32_t* idx,
+                             cudaStream_t s);
+constexpr int kMaxPlanChunks = 64;
+struct PlanBounds {
+    int64_t b[kMaxPlanChunks];   // leaf bounds b_0 <= ... <= b_{K-1} = n_leaves
+    int K;
+};
+cudaError_t launch_plan_ends(const uint32_t* sorted_keys, int64_t n, int64_t n_leaves, const PlanBounds& b,
+                             int64_t* chunk_end, int64_t* quant, cudaStream_t s);
 cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
-                            const double* aux, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
-                            cudaStream_t s);
+                            const double* aux, const Segments& sg, const RenderOpts& opt, float* grad_sigma,
+                            float* grad_sh, cudaStream_t s);
 cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
                          int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s);
 cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, int W, int H, float gamma,
                          unsigned long long* counters, cudaStream_t s);
 cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, float* dL_dC, double* loss,
                            cudaStream_t s);
-cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, const float* grad_sigma,
-                       const float* grad_sh, float lr, int64_t begin, int64_t end, cudaStream_t s);
+cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int64_t n_leaves, float* grad_sigma,
+                       float* grad_sh, float lr, int64_t begin, int64_t end, bool zero_grad, cudaStream_t s);
 
 }  // namespace po

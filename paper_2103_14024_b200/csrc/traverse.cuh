@@ -71,19 +71,27 @@ struct RayState {
 };
 
 // a1/a2: normalise d, move to grid units, slab-clip against [0, 2^D]^3.
-__device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], const float dir[3], RayState& r) {
-    // scale by the largest component first so tiny / huge directions normalise without
-    // under- or overflow; a zero or non-finite direction renders the background
+// Unit direction exactly as ray_setup computes it (the stored-segment pass 2 needs the same
+// SH basis as pass 1).  Scales by the largest component first so tiny / huge directions
+// normalise without under- or overflow; false for a zero / denormal / inf / NaN direction.
+__device__ __forceinline__ bool unit_direction(const float dir[3], float d[3]) {
     const float m = fmaxf(fabsf(dir[0]), fmaxf(fabsf(dir[1]), fabsf(dir[2])));
-    if (!(m >= 1.17549435e-38f) || !(m < INFINITY)) return false;   // zero / denormal / inf / NaN
+    if (!(m >= 1.17549435e-38f) || !(m < INFINITY)) return false;
     const float im = 1.0f / m;
     const float s0 = dir[0] * im, s1 = dir[1] * im, s2 = dir[2] * im;
     const float rn = im / sqrtf(s0 * s0 + s1 * s1 + s2 * s2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = dir[k] * rn;
+    return true;
+}
+
+__device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], const float dir[3], RayState& r) {
+    // a zero or non-finite direction renders the background
+    if (!unit_direction(dir, r.d)) return false;
     const float G = (float)(1 << tr.depth);
     float tn = 0.f, tf = INFINITY;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        r.d[k] = dir[k] * rn;
         r.o[k] = (o[k] - tr.bmin[k]) * tr.scale;
         r.dg[k] = r.d[k] * tr.scale;
         if (r.dg[k] != 0.f) {

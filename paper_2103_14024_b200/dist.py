@@ -9,6 +9,10 @@ SUMMED (reading Q23).  The gradient lives in one flat fp32 buffer
 which is split into contiguous buckets.  Each bucket is allreduced asynchronously (NCCL over
 NVLink/NVSwitch on a B200 box; gloo in the CPU tests) and the SGD update of a bucket's range
 can start as soon as that bucket has arrived, overlapping the remaining transfers.
+
+`overlapped_chunks` goes further: pass 2 runs in K chunks planned by
+po_backward_plan so that after chunk j the gradient of leaves [0, b_j) is final; that leaf
+range (its sigma~ slice and its SH slice of `flat`) is allreduced while chunks j+1.. run.
 Rendering needs no collective: views are sharded across ranks.
 """
 from __future__ import annotations
@@ -55,3 +59,41 @@ def flat_to_param_range(s: int, e: int, n_leaves: int, sh_offset: int) -> Tuple[
             return n_leaves
         return n_leaves + (x - sh_offset)
     return f(s), f(e)
+
+
+def leaf_range_slices(a: int, b: int, n_leaves: int, basis_dim: int, sh_offset: int):
+    """Leaves [a, b) -> ([flat ranges], [parameter ranges of po_tree_sgd_step_range])."""
+    ne = 3 * basis_dim
+    flat = [(a, b), (sh_offset + ne * a, sh_offset + ne * b)]
+    param = [(a, b), (n_leaves + ne * a, n_leaves + ne * b)]
+    return flat, param
+
+
+def overlapped_chunks(flat, leaf_end, n_leaves: int, basis_dim: int, sh_offset: int, run_chunk, apply_final,
+                      group=None, world_size: int = 1):
+    """Drive pass 2 chunk by chunk with the allreduce of each newly final leaf range.
+
+    run_chunk(j)        enqueue pass-2 chunk j (po_render_backward_chunk)
+    apply_final(b, e)   update parameter range [b, e) once its gradient is summed (SGD)
+    After chunk j every ray that writes leaves below leaf_end[j] has run (po_backward_plan),
+    so the range [leaf_end[j-1], leaf_end[j]) is allreduced asynchronously while the later
+    chunks are enqueued behind it; the updates follow in range order."""
+    import torch.distributed as dist
+    pending = []
+    prev = 0
+    for j, end in enumerate(leaf_end):
+        run_chunk(j)
+        fr, pr = leaf_range_slices(prev, int(end), n_leaves, basis_dim, sh_offset)
+        works = []
+        if world_size > 1:
+            for s, e in fr:
+                if e > s:
+                    works.append(dist.all_reduce(flat[s:e], op=dist.ReduceOp.SUM, group=group, async_op=True))
+        pending.append((works, pr))
+        prev = int(end)
+    for works, pr in pending:
+        for w in works:
+            w.wait()
+        for b, e in pr:
+            if e > b:
+                apply_final(b, e)

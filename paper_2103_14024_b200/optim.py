@@ -3,11 +3,18 @@
 One step on a ray batch, all compute in libplenoct kernels (this module only orders calls
 and owns buffers):
 
-  1. po_render_rays   forward + double-precision totals (pass 1 of P:949-957) -> rgb, aux
+  1. po_render_rays   forward + double-precision totals (pass 1 of P:949-957) -> rgb, aux,
+                      and (max_seg > 0) every sigma~>0 segment's (leaf, delta, w, T, c) stored
   2. po_l2_loss_grad  Eq. (3): dL/dC = 2 (C^ - C), loss = sum ||C^ - C||^2
-  3. po_render_backward  pass 2: per-leaf dL/dsigma~ and dL/dk scatter-added (+=)
+  3. po_render_backward  pass 2: per-leaf dL/dsigma~ and dL/dk scatter-added (+=), replaying the
+                      stored segments (re-traversing only rays with more than max_seg of them)
   4. SUM allreduce of the flat gradient in buckets (NCCL, only when world_size > 1)
   5. po_tree_sgd_step_range per bucket as soon as that bucket has landed (P:492, P:973 SGD)
+
+With chunks = K > 1 (the default when world_size > 1), steps 3-5 overlap:
+pass 1 also records each ray's leaf span, po_backward_plan orders the rays into K chunks,
+and the gradient range a chunk finalises is allreduced while the next chunks run
+(dist.overlapped_chunks).
 
 gamma defaults to 0: the paper applies early stopping "at test-time" (reading Q12).
 """
@@ -15,13 +22,14 @@ from __future__ import annotations
 
 import torch
 
-from . import (po_l2_loss_grad, po_render_backward, po_render_rays, po_tree_sgd_step_range)
-from .dist import allreduce_buckets, flat_layout, flat_to_param_range, plan_buckets
+from . import (Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk, po_render_rays,
+               po_tree_sgd_step_range)
+from .dist import allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets
 
 
 class OctreeOptimizer:
     def __init__(self, tree, lr: float, gamma: float = 0.0, background=(1.0, 1.0, 1.0), group=None,
-                 bucket_mb: float = 64.0, device=None):
+                 bucket_mb: float = 64.0, device=None, chunks=None, max_seg: int = 256):
         self.tree = tree
         self.lr = float(lr)
         self.gamma = float(gamma)
@@ -36,6 +44,12 @@ class OctreeOptimizer:
         self.buckets = plan_buckets(total, int(bucket_mb * (1 << 20)) // 4)
         self._bufs = {}
         self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+        # pass-2 chunks overlapped with the allreduce; None = 8 when world_size > 1, else 1
+        self.chunks = chunks
+        self._side = None
+        self.leaf_bounds = {}   # K -> host leaf bounds of po_backward_plan (calibrated on first use)
+        # stored pass-1 segments per ray (po_segments, max_seg * n * 32 B); 0 = re-traverse in pass 2
+        self.max_seg = int(max_seg)
 
     @property
     def world_size(self) -> int:
@@ -46,25 +60,77 @@ class OctreeOptimizer:
         if n not in self._bufs:
             self._bufs[n] = (torch.empty((n, 3), dtype=torch.float32, device=self.device),
                              torch.empty((n, 4), dtype=torch.float64, device=self.device),
-                             torch.empty((n, 3), dtype=torch.float32, device=self.device))
+                             torch.empty((n, 3), dtype=torch.float32, device=self.device),
+                             torch.empty((n, 2), dtype=torch.int32, device=self.device),
+                             torch.empty(n, dtype=torch.int32, device=self.device),
+                             Segments(n, self.max_seg, self.device) if self.max_seg > 0 else None)
         return self._bufs[n]
+
+    def n_chunks(self) -> int:
+        if self.chunks is not None:
+            return max(1, int(self.chunks))
+        return 8 if self.world_size > 1 else 1
 
     def step(self, rays: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
         """rays [n][6] f32, target [n][3] f32 on this rank's device; returns the local loss (device f64)."""
         n = rays.shape[0]
-        rgb, aux, dL = self._buffers(n)
-        po_render_rays(self.tree, rays, out=rgb, aux=aux, gamma=self.gamma, background=self.background)
+        rgb, aux, dL, span, perm, seg = self._buffers(n)
+        K = self.n_chunks()
+        po_render_rays(self.tree, rays, out=rgb, aux=aux, gamma=self.gamma, background=self.background,
+                       leaf_span=span if K > 1 else None, segments=seg)
         po_l2_loss_grad(rgb, target, dL_dC=dL, loss=self.loss)
-        self.flat.zero_()
-        po_render_backward(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux=aux, gamma=self.gamma,
-                           background=self.background)
+        # the gradient buffer is zero here: it starts zeroed and every SGD call below zeroes
+        # what it consumed (PO_SGD_ZERO_GRAD), which replaces a 0.7 GB memset per step
         nl = self.tree.n_leaves
+        if K > 1:
+            key = ("plan", K)
+            if key not in self._bufs:
+                self._bufs[key] = (torch.empty(K, dtype=torch.int64, device=self.device),
+                                   torch.empty(K, dtype=torch.int64, device=self.device))
+            ends, quant = self._bufs[key]
+            bounds = self.leaf_bounds.get(K)
+            _, ends, leaf_end = po_backward_plan(self.tree, span, K, leaf_bounds=bounds, perm=perm, chunk_ray_end=ends,
+                                                 key_quantiles=quant if bounds is None else None)
+            if bounds is None:
+                # first chunked step: one host sync to read this batch's ray quantiles; later
+                # steps reuse them as leaf bounds (equal-work chunks; batches of one scene
+                # have similar first-leaf distributions, and any bounds are correct)
+                self.leaf_bounds[K] = quant.cpu().tolist()
+            # chunks alternate between two side streams so one chunk's tail (its slowest rays)
+            # overlaps the next chunk; the current stream joins chunk j before the allreduce of
+            # the range chunk j finalises is enqueued on it (gradient atomics commute, so
+            # concurrent chunks are safe; only the allreduce needs chunks 0..j complete)
+            main = torch.cuda.current_stream(self.device)
+            if self._side is None:
+                self._side = [torch.cuda.Stream(self.device) for _ in range(2)]
+            ready = torch.cuda.Event()
+            ready.record(main)
+            for st in self._side:
+                st.wait_event(ready)
+
+            def run_chunk(j):
+                st = self._side[j % 2]
+                po_render_backward_chunk(self.tree, rays, perm, ends, j, dL, self.grad_sigma, self.grad_sh, aux=aux,
+                                         gamma=self.gamma, background=self.background, stream=st, segments=seg)
+                done = torch.cuda.Event()
+                done.record(st)
+                main.wait_event(done)
+
+            def apply_final(b, e):
+                po_tree_sgd_step_range(self.tree, self.grad_sigma, self.grad_sh, self.lr, b, e, zero_grad=True)
+
+            overlapped_chunks(self.flat, leaf_end, nl, self.tree.B, self.sh_off, run_chunk, apply_final,
+                              group=self.group, world_size=self.world_size)
+            return self.loss
+        po_render_backward(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux=aux, gamma=self.gamma,
+                           background=self.background, segments=seg)
         if self.world_size > 1:
             works = allreduce_buckets(self.flat, self.buckets, self.group)
             for (s, e), w in zip(self.buckets, works):
                 w.wait()   # makes the current stream wait for this bucket only
                 b, f = flat_to_param_range(s, e, nl, self.sh_off)
-                po_tree_sgd_step_range(self.tree, self.grad_sigma, self.grad_sh, self.lr, b, f)
+                po_tree_sgd_step_range(self.tree, self.grad_sigma, self.grad_sh, self.lr, b, f, zero_grad=True)
         else:
-            po_tree_sgd_step_range(self.tree, self.grad_sigma, self.grad_sh, self.lr, 0, nl * (1 + 3 * self.tree.B))
+            po_tree_sgd_step_range(self.tree, self.grad_sigma, self.grad_sh, self.lr, 0, nl * (1 + 3 * self.tree.B),
+                                   zero_grad=True)
         return self.loss

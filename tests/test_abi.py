@@ -83,5 +83,8 @@ def test_rejects_malformed_trees(po):
 
 def test_rejects_bad_args_without_gpu(po):
     o = po._opts(2.0, (1, 1, 1))   # gamma outside [0,1]
-    st = po.lib().po_render_rays(None, None, 1, ctypes.byref(o), None, None, None)
+    st = po.lib().po_render_rays(None, None, 1, ctypes.byref(o), None, None, None, None, None)
     assert st == 1
+    # chunk plan: NULL tree, bad K
+    assert po.lib().po_backward_plan(None, None, 1, 4, None, None, None, None, None, None) == 1
+    assert po.lib().po_render_backward_chunk(None, None, None, None, 0, None, None, None, None, None, None, None) == 1

@@ -246,41 +246,116 @@ def test_stats_match_oracle_c0(env, c0_tree):
 # ------------------------------------------------------------------------------------------
 # backward
 # ------------------------------------------------------------------------------------------
-def _backward_case(env, t, rays, gamma, use_aux, seed):
+def _backward_case(env, t, rays, gamma, use_aux, seed, chunks=0, max_seg=None):
+    """max_seg: None = re-traversing pass 2; an int = stored segments (po_segments) of that
+    capacity, rays with more sigma~>0 segments re-traverse (count = max_seg + 1)."""
     po, om, torch = env
     tree = po.tree_from_gen(t)
     r = _dev(torch, rays)
-    g = rng(seed).normal(size=(rays.shape[0], 3)).astype(np.float32)
+    n = rays.shape[0]
+    g = rng(seed).normal(size=(n, 3)).astype(np.float32)
     gs = torch.zeros(tree.n_leaves, device="cuda")
     gk = torch.zeros((tree.n_leaves, tree.B, 3), device="cuda")
     aux = None
-    if use_aux:
-        aux = torch.empty((rays.shape[0], 4), dtype=torch.float64, device="cuda")
-        po.po_render_rays(tree, r, aux=aux, gamma=gamma)
-    po.po_render_backward(tree, r, _dev(torch, g), gs, gk, aux=aux, gamma=gamma)
+    seg = po.Segments(n, max_seg) if max_seg is not None else None
+    if use_aux or chunks or seg is not None:
+        aux = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+        span = torch.empty((n, 2), dtype=torch.int32, device="cuda") if chunks else None
+        po.po_render_rays(tree, r, aux=aux, gamma=gamma, leaf_span=span, segments=seg)
+    if seg is not None:
+        cnt = seg.count.cpu().numpy()
+        assert cnt.min() >= 0 and cnt.max() <= max_seg + 1
+    if chunks:   # pass 2 through po_backward_plan + po_render_backward_chunk (a8/a9 overlap)
+        perm, ends, _ = po.po_backward_plan(tree, span, chunks)
+        for j in range(chunks):
+            po.po_render_backward_chunk(tree, r, perm, ends, j, _dev(torch, g), gs, gk, aux=aux, gamma=gamma,
+                                        segments=seg)
+    else:
+        po.po_render_backward(tree, r, _dev(torch, g), gs, gk, aux=aux, gamma=gamma, segments=seg)
     rs, rk = om.backward(om.OracleTree(t), rays.astype(np.float64), g.astype(np.float64), gamma=gamma)
     _grad_ok(gs.cpu().numpy(), rs, "sigma")
     _grad_ok(gk.cpu().numpy(), rk, "sh")
 
 
-@pytest.mark.parametrize("gamma,use_aux", [(0.0, False), (0.0, True), (0.01, False), (0.01, True)])
-def test_c0_backward(env, c0_tree, gamma, use_aux):
+@pytest.mark.parametrize("gamma,use_aux,chunks,max_seg", [
+    (0.0, False, 0, None), (0.0, True, 0, None), (0.01, False, 0, None), (0.01, True, 0, None),
+    (0.0, True, 5, None), (0.01, True, 3, None),
+    (0.0, True, 0, 64), (0.01, True, 0, 64), (0.0, True, 0, 3), (0.0, True, 4, 3), (0.0, True, 0, 0)])
+def test_c0_backward(env, c0_tree, gamma, use_aux, chunks, max_seg):
     po, om, torch = env
     cam, W, H = gen.config_camera("c0")
     rays = om.camera_rays(cam, W, H)
     ot = om.OracleTree(c0_tree)
     ok = _tie_free(om, ot, rays, gamma)
-    _backward_case(env, c0_tree, rays[ok].astype(np.float32), gamma, use_aux, 21)
+    _backward_case(env, c0_tree, rays[ok].astype(np.float32), gamma, use_aux, 21, chunks, max_seg)
 
 
-@pytest.mark.parametrize("seed,deg", [(31, 1), (32, 2), (33, 3), (34, 0)])
-def test_random_tree_backward(env, seed, deg):
+@pytest.mark.parametrize("gamma", [0.0, 0.01])
+def test_leaf_span_matches_oracle(env, gamma):
+    """po_render_rays leaf_span = [min, max] index of the sigma~ > 0 leaves the oracle's ray
+    composites (the leaves its backward writes), (0xFFFFFFFF, 0) for none."""
+    po, om, torch = env
+    t = gen.scene_random(41, depth=5, sh_degree=1, sigma_scale=3.0)
+    rays = gen.random_rays(42, 3000, inside_frac=0.1)
+    ot = om.OracleTree(t)
+    ok = _tie_free(om, ot, rays.astype(np.float64), gamma if gamma > 0 else 1e-30)
+    rays = rays[ok]
+    tree = po.tree_from_gen(t)
+    n = rays.shape[0]
+    aux = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+    span = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+    po.po_render_rays(tree, _dev(torch, rays), aux=aux, gamma=gamma, leaf_span=span)
+    got = span.cpu().numpy().view(np.uint32)
+    ref = om.render(ot, rays.astype(np.float64), gamma=gamma, max_leaves=256)
+    for i in range(n):
+        ids = ref["leaf_ids"][i, :ref["n_proc"][i]]
+        ids = ids[t.sigma[ids] > 0]
+        want = (ids.min(), ids.max()) if ids.size else (0xFFFFFFFF, 0)
+        assert tuple(got[i]) == tuple(int(x) for x in want), i
+
+
+def test_backward_plan_exact(env):
+    """po_backward_plan against its definition written out (tests/test_dist_cpu.emulate_plan):
+    stable sort by lowest leaf, chunk ends = #keys < b_j (uniform or caller bounds), quantiles
+    of the sorted keys; bit-exact.  Bad bounds are rejected."""
+    po, om, torch = env
+    from test_dist_cpu import emulate_plan
+    t = gen.scene_random(43, depth=4, sh_degree=0)
+    tree = po.tree_from_gen(t)
+    nl = tree.n_leaves
+    g = rng(44)
+    for n, K, custom in ((1, 1, False), (1000, 7, False), (100000, 8, True), (33, 64, False), (5000, 3, True)):
+        lo = g.integers(0, nl, size=n).astype(np.uint32)
+        lo[g.random(n) < 0.1] = 0xFFFFFFFF   # rays with no sigma>0 leaf
+        hi = np.where(lo == 0xFFFFFFFF, 0, lo).astype(np.uint32)
+        span = torch.from_numpy(np.stack([lo, hi], 1).view(np.int32).copy()).cuda()
+        bounds = None
+        if custom:
+            bounds = sorted(g.integers(0, nl + 1, size=K - 1).tolist()) + [nl]
+        q = torch.empty(K, dtype=torch.int64, device="cuda")
+        perm, ends, leaf_end = po.po_backward_plan(tree, span, K, leaf_bounds=bounds, key_quantiles=q)
+        p_ref, e_ref, l_ref, q_ref = emulate_plan(lo.astype(np.int64), nl, K, bounds)
+        assert leaf_end == l_ref
+        assert ends.cpu().tolist() == e_ref
+        assert q.cpu().tolist() == q_ref
+        np.testing.assert_array_equal(perm.cpu().numpy(), p_ref)
+    span = torch.zeros((4, 2), dtype=torch.int32, device="cuda")
+    for bad in ([nl, nl - 1, nl], [0, 1, nl - 1], [-1, 0, nl]):
+        with pytest.raises(po.PoError):
+            po.po_backward_plan(tree, span, 3, leaf_bounds=bad)
+    with pytest.raises(po.PoError):
+        po.po_backward_plan(tree, span, 65)
+
+
+@pytest.mark.parametrize("seed,deg,max_seg", [(31, 1, None), (32, 2, None), (33, 3, None), (34, 0, None),
+                                              (35, 3, 8), (36, 1, 8)])
+def test_random_tree_backward(env, seed, deg, max_seg):
     po, om, torch = env
     t = gen.scene_random(seed, depth=5, sh_degree=deg)
     rays = gen.random_rays(seed, 2000, inside_frac=0.1)
     ot = om.OracleTree(t)
     ok = _tie_free(om, ot, rays.astype(np.float64), 1e-30)
-    _backward_case(env, t, rays[ok], 0.0, False, seed)
+    _backward_case(env, t, rays[ok], 0.0, False, seed, max_seg=max_seg)
 
 
 def test_backward_fd_c0(env, c0_tree):
@@ -345,8 +420,46 @@ def test_loss_grad_and_sgd(env):
         po.po_tree_sgd_step(tq, gs, gk, 0.25)
 
 
-def test_optimizer_step_matches_oracle(env):
-    """a7..a9 chain (OctreeOptimizer.step, world size 1) vs the oracle's Eq. (3) gradient + SGD."""
+@pytest.mark.parametrize("deg", [0, 1, 3])
+def test_sgd_range_sparse_and_zeroing(env, deg):
+    """po_tree_sgd_step_range over ragged ranges (quad path + scalar head/tail, ne = 3 / 12 / 48):
+    p -= lr g exactly where g != 0, untouched where g == 0, and PO_SGD_ZERO_GRAD zeroes exactly
+    the consumed range."""
+    po, om, torch = env
+    t = gen.scene_random(51 + deg, depth=4, sh_degree=deg)
+    tree = po.tree_from_gen(t)
+    nl, B = tree.n_leaves, tree.B
+    total = nl * (1 + 3 * B)
+    g = rng(52)
+    gs = torch.from_numpy(g.normal(size=nl).astype(np.float32))
+    gk = torch.from_numpy(g.normal(size=(nl, B, 3)).astype(np.float32))
+    gs[g.random(nl) < 0.3] = 0.0
+    gk[torch.from_numpy(g.random(nl) < 0.3)] = 0.0   # whole untouched rows
+    flat_ref = np.concatenate([gs.numpy(), gk.numpy().reshape(-1)]).astype(np.float64)
+    p_ref = np.concatenate([t.sigma.astype(np.float64), t.sh.astype(np.float64).reshape(-1)])
+    gs_d, gk_d = gs.cuda(), gk.cuda()
+    cuts = sorted(set([0, total] + g.integers(0, total, size=6).tolist() + [nl, nl + 5, nl + 3 * B * 7 + 1]))
+    cuts = [c for c in cuts if 0 <= c <= total]
+    lr = 0.5
+    untouched = flat_ref == 0.0
+    p0 = p_ref.copy()
+    for k, (b, e) in enumerate(zip(cuts, cuts[1:])):
+        po.po_tree_sgd_step_range(tree, gs_d, gk_d, lr, b, e, zero_grad=(k % 2 == 0))
+        p_ref[b:e] = p_ref[b:e] - lr * flat_ref[b:e]
+        if k % 2 == 0:
+            flat_ref[b:e] = 0.0
+    s1, k1 = tree.read_leaves()
+    got = np.concatenate([s1.astype(np.float64), k1.astype(np.float64).reshape(-1)])
+    np.testing.assert_allclose(got, p_ref, rtol=1e-6, atol=1e-6)   # one fp32 rounding (or FMA)
+    np.testing.assert_array_equal(got[untouched], p0[untouched])
+    flat = np.concatenate([gs_d.cpu().numpy(), gk_d.cpu().numpy().reshape(-1)])
+    np.testing.assert_array_equal(flat, flat_ref.astype(np.float32))
+
+
+@pytest.mark.parametrize("chunks,max_seg", [(1, 0), (5, 0), (1, 16), (5, 16)])
+def test_optimizer_step_matches_oracle(env, chunks, max_seg):
+    """a7..a9 chain (OctreeOptimizer.step, world size 1) vs the oracle's Eq. (3) gradient + SGD;
+    chunks = 5 runs pass 2 + SGD through po_backward_plan's chunks (the overlapped path)."""
     po, om, torch = env
     from paper_2103_14024_b200.optim import OctreeOptimizer
     t = gen.scene_random(60, depth=5, sh_degree=3, sigma_scale=3.0)
@@ -358,12 +471,13 @@ def test_optimizer_step_matches_oracle(env):
     target = rng(62).random((rays.shape[0], 3)).astype(np.float32)
     tree = po.tree_from_gen(t)
     lr = 1.0   # large enough that fp32 rounding of the updated leaves does not mask the gradient
-    opt = OctreeOptimizer(tree, lr=lr, gamma=0.0)
+    opt = OctreeOptimizer(tree, lr=lr, gamma=0.0, chunks=chunks, max_seg=max_seg)
     loss = opt.step(_dev(torch, rays), _dev(torch, target)).item()
     ref = om.render(ot, r64, gamma=0.0)
     diff = ref["rgb"] - target.astype(np.float64)
     assert abs(loss - (diff ** 2).sum()) <= 1e-5 * (diff ** 2).sum()
     gs, gk = om.backward(ot, r64, 2.0 * diff, gamma=0.0)
+    assert not opt.flat.any().item()   # every SGD range zeroed the gradient it consumed
     s1, k1 = tree.read_leaves()
     _grad_ok((t.sigma.astype(np.float64) - s1) / lr, gs, "sgd sigma")
     _grad_ok((t.sh.astype(np.float64) - k1) / lr, gk, "sgd sh")
