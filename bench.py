@@ -482,7 +482,7 @@ def main():
     ap.add_argument("--max-seg", type=int, default=256,
                     help="c4: stored pass-1 segments per ray (0 = pass 2 re-traverses every ray)")
     ap.add_argument("--chunks", type=int, default=None,
-                    help="c4: pass-2 chunks overlapped with the allreduce (default 8 if N>1, else 1)")
+                    help="c4: pass-2 chunks overlapped with the allreduce (default 4 if N>1, else 1)")
     ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
     ap.add_argument("--ray-order", choices=["sampled", "leaf"], default="leaf",

@@ -11,7 +11,7 @@ and owns buffers):
   4. SUM allreduce of the flat gradient in buckets (NCCL, only when world_size > 1)
   5. po_tree_sgd_step_range per bucket as soon as that bucket has landed (P:492, P:973 SGD)
 
-With chunks = K > 1 (the default when world_size > 1), steps 3-5 overlap:
+With chunks = K > 1 (K = 4 by default when world_size > 1), steps 3-5 overlap:
 pass 1 also records each ray's leaf span, po_backward_plan orders the rays into K chunks,
 and the gradient range a chunk finalises is allreduced while the next chunks run
 (dist.overlapped_chunks).
@@ -44,7 +44,7 @@ class OctreeOptimizer:
         self.buckets = plan_buckets(total, int(bucket_mb * (1 << 20)) // 4)
         self._bufs = {}
         self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
-        # pass-2 chunks overlapped with the allreduce; None = 8 when world_size > 1, else 1
+        # pass-2 chunks overlapped with the allreduce; None = 4 when world_size > 1, else 1
         self.chunks = chunks
         self._side = None
         self.leaf_bounds = {}   # K -> host leaf bounds of po_backward_plan (calibrated on first use)
@@ -69,7 +69,7 @@ class OctreeOptimizer:
     def n_chunks(self) -> int:
         if self.chunks is not None:
             return max(1, int(self.chunks))
-        return 8 if self.world_size > 1 else 1
+        return 4 if self.world_size > 1 else 1
 
     def step(self, rays: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
         """rays [n][6] f32, target [n][3] f32 on this rank's device; returns the local loss (device f64)."""
