@@ -219,6 +219,24 @@ po_status po_tree_sgd_step(po_tree* tree, const float* grad_sigma, const float* 
 po_status po_tree_sgd_step_range(po_tree* tree, float* grad_sigma, float* grad_sh, float lr, int64_t begin,
                                  int64_t end, int32_t flags, po_stream stream);
 
+/* ---- NEXT rows on the same traversal ------------------------------------
+ * po_render_depth (f4; "render the depth map", alpha maps P:468; reading Q34):
+ *   alpha[i] = 1 - T_stop and depth[i] = sum_i w_i (t_in,i + t_out,i) / 2 over the segments
+ *   composited up to termination (w_i as in Eq. 1-2, t in world units along the unit
+ *   direction from the ray origin; the background adds nothing, so depth / alpha is the
+ *   normalised depth).  rays device float[n][6]; alpha, depth device float[n]; sigma~ only.
+ * po_leaf_max_alpha (f1, visibility filtering; reading Q33): for every leaf a ray
+ *   composites before it terminates (opts->gamma), max_alpha[leaf] = max(max_alpha[leaf],
+ *   1 - exp(-sigma delta)) -- "the maximum ray weight ... at each voxel" -- over all n rays.
+ *   max_alpha device float[n_leaves], MAX-accumulated: the caller initialises it with values
+ *   >= 0 (the max is taken on the IEEE bit patterns, which order like non-negative floats; 0 for a
+ *   fresh pass) and may accumulate over several calls (all training views).  Leaves whose
+ *   maximum stays below tau_w are the ones the paper removes. */
+po_status po_render_depth(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
+                          float* alpha, float* depth, po_stream stream);
+po_status po_leaf_max_alpha(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
+                            float* max_alpha, po_stream stream);
+
 /* ---- parity / measurement helpers ----------------------------------------------------
  * po_trace: the visited-leaf sequence of each ray up to termination (same traversal as
  * po_render_rays).  leaf_ids device int32[n][max_leaves] (first max_leaves, -1 padded;

@@ -54,6 +54,8 @@ def lib():
         _lib.or_render.argtypes = [P, P, I64, D, P, ctypes.c_int, P, P, P, I32, P, P, ctypes.c_int]
         _lib.or_backward.argtypes = [P, P, I64, D, P, P, P, P, ctypes.c_int, P, P]
         _lib.or_tie_flags.argtypes = [P, P, I64, D, D, D, P, ctypes.c_int]
+        _lib.or_render_depth.argtypes = [P, P, I64, D, P, P, ctypes.c_int]
+        _lib.or_leaf_max_alpha.argtypes = [P, P, I64, D, P, ctypes.c_int]
     return _lib
 
 
@@ -133,6 +135,23 @@ def render(ot: OracleTree, rays, gamma: float = 0.01, bg=(1.0, 1.0, 1.0), mode: 
     lib().or_render(ot.ref, _ptr(rays), n, gamma, _ptr(bg), mode, _ptr(rgb), _ptr(T), _ptr(n_proc), max_leaves,
                     _ptr(ids), _ptr(nodes), nthreads)
     return dict(rgb=rgb, T=T, n_proc=n_proc, nodes_met=nodes, leaf_ids=ids)
+
+
+def render_depth(ot: OracleTree, rays, gamma: float = 0.01, nthreads: int = 0):
+    """NEXT f4: (alpha [n], depth [n]) = (1 - T_stop, sum_i w_i (t_in + t_out) / 2), reading Q34."""
+    rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
+    a = np.zeros(rays.shape[0])
+    d = np.zeros(rays.shape[0])
+    lib().or_render_depth(ot.ref, _ptr(rays), rays.shape[0], gamma, _ptr(a), _ptr(d), nthreads)
+    return a, d
+
+
+def leaf_max_alpha(ot: OracleTree, rays, gamma: float = 0.01, nthreads: int = 0) -> np.ndarray:
+    """NEXT f1: per-leaf max over rays of 1 - exp(-sigma delta), reading Q33."""
+    rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
+    m = np.zeros(ot.n_leaves)
+    lib().or_leaf_max_alpha(ot.ref, _ptr(rays), rays.shape[0], gamma, _ptr(m), nthreads)
+    return m
 
 
 def backward(ot: OracleTree, rays, dL_dC, gamma: float = 0.0, bg=(1.0, 1.0, 1.0), nthreads: int = 0,

@@ -509,6 +509,79 @@ int or_backward(const or_tree* T, const double* rays, int64_t n, double gamma, c
     return 0;
 }
 
+// NEXT f4 ("render the depth map"; alpha maps P:468): per ray, over the segments
+// composited up to termination (Eq. 1-2 weights w_i = T_i (1 - exp(-sigma_i delta_i))):
+//   alpha = 1 - T_stop,   depth = sum_i w_i (t_in,i + t_out,i) / 2     (reading Q34)
+// t in world units from the ray origin along the unit direction; the background adds 0.
+int or_render_depth(const or_tree* T, const double* rays, int64_t n, double gamma, double* alpha, double* depth,
+                    int nthreads) {
+    int nt = set_threads(nthreads);
+#pragma omp parallel num_threads(nt)
+    {
+        Ctx cx;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            Ray r = make_ray(rays + i * 6);
+            double tn, tf;
+            bool hit;
+            segments(T, r, 0, nullptr, cx, &tn, &tf, &hit);
+            double Tr = 1.0, D = 0.0;
+            if (hit) {
+                for (const Seg& s : cx.segs) {
+                    double sig = std::max((double)T->sigma[s.leaf], 0.0);
+                    double delta = s.t1 - s.t0;
+                    double w = Tr * -std::expm1(-sig * delta);
+                    D += w * 0.5 * (s.t0 + s.t1);
+                    Tr = Tr * std::exp(-sig * delta);
+                    if (Tr < gamma) break;
+                }
+            }
+            alpha[i] = 1.0 - Tr;
+            depth[i] = D;
+        }
+    }
+    return 0;
+}
+
+// NEXT f1, visibility filtering: "keeping track of the maximum ray weight
+// 1 - exp(-sigma_i delta_i) at each voxel" over the leaves each ray composites before it
+// terminates (reading Q33).  max_alpha [n_leaves] is max-accumulated (caller initialises).
+int or_leaf_max_alpha(const or_tree* T, const double* rays, int64_t n, double gamma, double* max_alpha,
+                      int nthreads) {
+    int nt = set_threads(nthreads);
+    std::vector<std::vector<double>> part((size_t)nt);
+#pragma omp parallel num_threads(nt)
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        std::vector<double>& mine = part[(size_t)tid];
+        mine.assign((size_t)T->n_leaves, 0.0);
+        Ctx cx;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            Ray r = make_ray(rays + i * 6);
+            double tn, tf;
+            bool hit;
+            segments(T, r, 0, nullptr, cx, &tn, &tf, &hit);
+            if (!hit) continue;
+            double Tr = 1.0;
+            for (const Seg& s : cx.segs) {
+                double sig = std::max((double)T->sigma[s.leaf], 0.0);
+                double delta = s.t1 - s.t0;
+                double a = -std::expm1(-sig * delta);   // 1 - exp(-sigma delta)
+                mine[(size_t)s.leaf] = std::max(mine[(size_t)s.leaf], a);
+                Tr = Tr * std::exp(-sig * delta);
+                if (Tr < gamma) break;
+            }
+        }
+    }
+    for (const std::vector<double>& v : part)
+        for (size_t j = 0; j < v.size(); ++j) max_alpha[j] = std::max(max_alpha[j], v[j]);
+    return 0;
+}
+
 // Tie tags (reading Q27).  bit0: two level-D plane crossings (or t_near / t_far) inside
 // [t_near, t_far] closer than tol_plane*edge; bit1: a processed delta < tol_plane*edge;
 // bit2: some T_{i+1} within tol_gamma*gamma of gamma; bit3: origin inside the box within

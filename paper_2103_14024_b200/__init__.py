@@ -26,7 +26,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_destroy", "po_tree_info",
            "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_backward_plan", "po_render_backward_chunk",
-           "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
+           "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
            "po_render_timeline"]
 
 
@@ -94,6 +94,8 @@ def lib():
         L.po_backward_plan.argtypes = [P, P, I64, I32, P, P, P, P, P, P]
         L.po_render_backward_chunk.argtypes = [P, P, P, P, I32, P, P, P, P, P, P, P]
         L.po_camera_rays.argtypes = [P, I32, I32, I32, P, I32, P]
+        L.po_render_depth.argtypes = [P, P, I64, P, P, P, P]
+        L.po_leaf_max_alpha.argtypes = [P, P, I64, P, P, P]
         L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P, P]
         L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
         L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
@@ -328,6 +330,36 @@ def po_render_backward(tree: PlenOctree, rays, dL_dC, grad_sigma, grad_sh, aux=N
     o = _opts(gamma, background)
     _check(lib().po_render_backward(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux), _seg(segments),
                                     ctypes.byref(o), _ptr(grad_sigma), _ptr(grad_sh), _stream(stream)))
+
+
+def po_render_depth(tree: PlenOctree, rays, gamma: float = 0.01, alpha=None, depth=None, stream=None):
+    """NEXT f4: (alpha [n], depth [n]) maps of explicit rays (include/plenoct.h, reading Q34)."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    n = rays.shape[0]
+    if alpha is None:
+        alpha = torch.empty(n, dtype=torch.float32, device=rays.device)
+    if depth is None:
+        depth = torch.empty(n, dtype=torch.float32, device=rays.device)
+    _need(alpha, torch.float32)
+    _need(depth, torch.float32)
+    o = _opts(gamma, (1.0, 1.0, 1.0))
+    _check(lib().po_render_depth(tree.handle, _ptr(rays), n, ctypes.byref(o), _ptr(alpha), _ptr(depth),
+                                 _stream(stream)))
+    return alpha, depth
+
+
+def po_leaf_max_alpha(tree: PlenOctree, rays, max_alpha=None, gamma: float = 0.01, stream=None):
+    """NEXT f1: max-accumulates 1 - exp(-sigma delta) per leaf over the rays (reading Q33)."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    if max_alpha is None:
+        max_alpha = torch.zeros(tree.n_leaves, dtype=torch.float32, device=rays.device)
+    _need(max_alpha, torch.float32)
+    o = _opts(gamma, (1.0, 1.0, 1.0))
+    _check(lib().po_leaf_max_alpha(tree.handle, _ptr(rays), rays.shape[0], ctypes.byref(o), _ptr(max_alpha),
+                                   _stream(stream)))
+    return max_alpha
 
 
 def po_l2_loss_grad(pred, target, dL_dC=None, loss=None, stream=None):

@@ -777,6 +777,34 @@ po_status po_trace(const po_tree* t, const float* rays, int64_t n, const po_rend
                     "po_trace");
 }
 
+po_status po_render_depth(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, float* alpha,
+                          float* depth, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (n == 0) return PO_OK;
+    if (!rays || !alpha || !depth) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_render_depth(dev_tree(t), rays, n, o.gamma, alpha, depth, (cudaStream_t)stream),
+                    "po_render_depth");
+}
+
+po_status po_leaf_max_alpha(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts,
+                            float* max_alpha, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (n == 0) return PO_OK;
+    if (!rays || !max_alpha) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_leaf_max_alpha(dev_tree(t), rays, n, o.gamma, max_alpha, (cudaStream_t)stream),
+                    "po_leaf_max_alpha");
+}
+
 po_status po_render_timeline(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                              const po_render_opts* opts, float* out_rgb, unsigned long long* timeline,
                              po_stream stream) {

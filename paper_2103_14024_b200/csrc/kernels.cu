@@ -281,6 +281,41 @@ struct GradVisitor {
     }
 };
 
+// NEXT f4 (P:638 depth map, P:468 alpha map; reading Q34): alpha = 1 - T_stop and the
+// expected depth sum_i w_i (t_in + t_out) / 2 over the composited segments.  sigma~ only:
+// no SH rows are read.
+struct DepthVisitor {
+    const DevTree& tr;
+    float T, gamma, D;
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+        D = fmaf(a.w, 0.5f * (t0 + t1), D);
+        T = a.Tn;
+        return !(T < gamma);
+    }
+};
+
+// NEXT f1, visibility filtering (reading Q33): per-leaf maximum over rays of the
+// ray weight 1 - exp(-sigma delta) for every leaf composited before termination.  alpha >= 0,
+// so the IEEE bit pattern orders like the value and atomicMax on it is a float max.
+struct MaxAlphaVisitor {
+    const DevTree& tr;
+    float T, gamma;
+    unsigned* __restrict__ max_alpha;
+    __device__ __forceinline__ void on_node() {}
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        const float st = __ldg(tr.sigma + idx);
+        if (!(st > 0.f)) return true;   // alpha = 0: the maximum is unchanged
+        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
+        atomicMax(max_alpha + idx, __float_as_uint(__fsub_rn(1.0f, a.e)));
+        T = a.Tn;
+        return !(T < gamma);
+    }
+};
+
 struct TraceVisitor {
     const DevTree& tr;
     float T, gamma;
@@ -776,6 +811,41 @@ __global__ void k_plan_ends(const uint32_t* __restrict__ sorted_keys, int64_t n,
     }
 }
 
+__global__ void __launch_bounds__(256) k_render_depth(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                      float gamma, float* __restrict__ alpha,
+                                                      float* __restrict__ depth) {
+    PO_DECLARE_STACK(stk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __ldg(rays + i * 6 + k);
+        d[k] = __ldg(rays + i * 6 + 3 + k);
+    }
+    DepthVisitor v{tr, 1.f, gamma, 0.f};
+    RayState r;
+    if (ray_setup(tr, o, d, r)) traverse(tr, r, v, stk);
+    alpha[i] = __fsub_rn(1.0f, v.T);
+    depth[i] = v.D;
+}
+
+__global__ void __launch_bounds__(256) k_leaf_max_alpha(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                        float gamma, unsigned* __restrict__ max_alpha) {
+    PO_DECLARE_STACK(stk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __ldg(rays + i * 6 + k);
+        d[k] = __ldg(rays + i * 6 + 3 + k);
+    }
+    MaxAlphaVisitor v{tr, 1.f, gamma, max_alpha};
+    RayState r;
+    if (ray_setup(tr, o, d, r)) traverse(tr, r, v, stk);
+}
+
 __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restrict__ rays, int64_t n, float gamma,
                                                int32_t max_leaves, int32_t* __restrict__ leaf_ids,
                                                int32_t* __restrict__ counts, int32_t* __restrict__ node_counts) {
@@ -1101,6 +1171,22 @@ cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* r
                                                                        grad_sh);
         }
     });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_render_depth(const DevTree& tr, const float* rays, int64_t n, float gamma, float* alpha,
+                                float* depth, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    carveout_once(k_render_depth);
+    k_render_depth<<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, alpha, depth);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_leaf_max_alpha(const DevTree& tr, const float* rays, int64_t n, float gamma, float* max_alpha,
+                                  cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    carveout_once(k_leaf_max_alpha);
+    k_leaf_max_alpha<<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, reinterpret_cast<unsigned*>(max_alpha));
     return cudaGetLastError();
 }
 

@@ -48,6 +48,10 @@ cudaError_t launch_plan_ends(const uint32_t* sorted_keys, int64_t n, int64_t n_l
 cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
                             const double* aux, const Segments& sg, const RenderOpts& opt, float* grad_sigma,
                             float* grad_sh, cudaStream_t s);
+cudaError_t launch_render_depth(const DevTree& tr, const float* rays, int64_t n, float gamma, float* alpha,
+                                float* depth, cudaStream_t s);
+cudaError_t launch_leaf_max_alpha(const DevTree& tr, const float* rays, int64_t n, float gamma, float* max_alpha,
+                                  cudaStream_t s);
 cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
                          int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s);
 cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, int W, int H, float gamma,

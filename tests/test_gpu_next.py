@@ -1,0 +1,101 @@
+"""GPU parity of the NEXT rows against the pinned oracle:
+f4 alpha / expected-depth maps (po_render_depth, reading Q34) and f1 visibility filtering
+(po_leaf_max_alpha, reading Q33).  Tie-free rays only (reading Q27); the bars are
+the forward's: 1e-4 absolute on alpha and on depth / max(1, |depth|)."""
+import numpy as np
+import pytest
+
+import gen
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def env(oracle_mod):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as g
+    g.build()
+    import paper_2103_14024_b200 as po
+    return po, oracle_mod, torch
+
+
+def _tie_free(om, ot, rays, gamma):
+    return om.tie_flags(ot, rays, gamma=gamma if gamma > 0 else 1e-30) == 0
+
+
+def _cases():
+    return [("c0", 0.01), ("c0", 0.0), ("random", 0.01), ("random", 0.0)]
+
+
+def _scene(name):
+    if name == "c0":
+        t = gen.scene_c0()
+        cam, W, H = gen.config_camera("c0")
+        return t, cam, W, H, None
+    t = gen.scene_random(71, depth=6, sh_degree=1, sigma_scale=3.0)
+    return t, None, 0, 0, gen.random_rays(72, 4000, inside_frac=0.1).astype(np.float64)
+
+
+@pytest.mark.parametrize("name,gamma", _cases())
+def test_depth_alpha_match_oracle(env, name, gamma):
+    po, om, torch = env
+    t, cam, W, H, rays = _scene(name)
+    ot = om.OracleTree(t)
+    if rays is None:
+        rays = om.camera_rays(cam, W, H)
+    rays = rays[_tie_free(om, ot, rays, gamma)]
+    tree = po.tree_from_gen(t)
+    a, d = po.po_render_depth(tree, torch.from_numpy(rays.astype(np.float32)).cuda(), gamma=gamma)
+    # the oracle sees the fp32 rays the GPU sees
+    ra, rd = om.render_depth(ot, rays.astype(np.float32).astype(np.float64), gamma=gamma)
+    a, d = a.cpu().numpy(), d.cpu().numpy()
+    assert np.abs(a - ra).max() <= TOL
+    assert (np.abs(d - rd) / np.maximum(1.0, np.abs(rd))).max() <= TOL
+    assert (ra > 0.5).any()   # the case actually hits something
+
+
+@pytest.mark.parametrize("name,gamma", _cases())
+def test_leaf_max_alpha_matches_oracle(env, name, gamma):
+    po, om, torch = env
+    t, cam, W, H, rays = _scene(name)
+    ot = om.OracleTree(t)
+    if rays is None:
+        rays = om.camera_rays(cam, W, H)
+    rays = rays[_tie_free(om, ot, rays, gamma)].astype(np.float32)
+    tree = po.tree_from_gen(t)
+    r = torch.from_numpy(rays).cuda()
+    got = po.po_leaf_max_alpha(tree, r, gamma=gamma).cpu().numpy()
+    want = om.leaf_max_alpha(ot, rays.astype(np.float64), gamma=gamma)
+    assert np.abs(got - want).max() <= TOL
+    assert (want > 0).sum() > 100
+    # max-accumulation across calls (several training views): two halves == one pass
+    half = rays.shape[0] // 2
+    acc = po.po_leaf_max_alpha(tree, r[:half].contiguous(), gamma=gamma)
+    po.po_leaf_max_alpha(tree, r[half:].contiguous(), max_alpha=acc, gamma=gamma)
+    np.testing.assert_array_equal(acc.cpu().numpy(), got)
+
+
+def test_c1_depth_and_filter_sampled(env, c1_tree):
+    """c1 scale: 20,000 random pixels of view 0 (tie-free), depth/alpha and the filter
+    statistic of the leaves they reach."""
+    po, om, torch = env
+    cam, W, H = gen.config_camera("c1", 0)
+    g = np.random.default_rng(5)
+    pix = g.choice(W * H, 20000, replace=False)
+    rays = om.camera_rays(cam, W, H)[pix]
+    ot = om.OracleTree(c1_tree)
+    rays = rays[_tie_free(om, ot, rays, 0.01)].astype(np.float32)
+    tree = po.tree_from_gen(c1_tree)
+    r = torch.from_numpy(rays).cuda()
+    a, d = po.po_render_depth(tree, r, gamma=0.01)
+    ra, rd = om.render_depth(ot, rays.astype(np.float64), gamma=0.01)
+    assert np.abs(a.cpu().numpy() - ra).max() <= 2e-3   # c1 sigma up to 768 (reading Q26)
+    assert (np.abs(d.cpu().numpy() - rd) / np.maximum(1.0, np.abs(rd))).max() <= 2e-3
+    got = po.po_leaf_max_alpha(tree, r, gamma=0.01).cpu().numpy()
+    want = om.leaf_max_alpha(ot, rays.astype(np.float64), gamma=0.01)
+    assert np.abs(got - want).max() <= 2e-3
+    assert ((got > 0) == (want > 0)).mean() > 0.999
