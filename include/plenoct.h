@@ -31,7 +31,7 @@ typedef enum {
     PO_ERR_INVALID_TREE = 2,  /* malformed child table, NaN/Inf payload, leaf deeper than D  */
     PO_ERR_OOM = 3,           /* cudaMalloc failed                                           */
     PO_ERR_CUDA = 4,          /* any other CUDA runtime error                                */
-    PO_ERR_UNSUPPORTED = 5    /* sh_degree > 3, unknown payload, op not defined for payload  */
+    PO_ERR_UNSUPPORTED = 5    /* sh_degree > 4, unknown payload, op not defined for payload  */
 } po_status;
 
 enum { PO_F32 = 0, PO_F16 = 1 };          /* leaf SH payload precision (sigma~ is always f32, reading Q20) */
@@ -46,7 +46,7 @@ typedef struct {
     float bbox_min[3];
     float bbox_edge;      /* > 0, world units                                  */
     int32_t max_depth;    /* D, 1..15                                          */
-    int32_t sh_degree;    /* l_max, 0..3 ; B = (l_max+1)^2 coefficients/channel */
+    int32_t sh_degree;    /* l_max, 0..4 (4 = SH-25); B = (l_max+1)^2 coefs/channel */
     int32_t payload;      /* PO_F32 | PO_F16                                   */
     int32_t sh_sign;      /* PO_SH_CS | PO_SH_NO_CS                            */
     int32_t device;       /* CUDA ordinal the tree lives on                    */

@@ -245,8 +245,8 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
         if (!std::isfinite(desc->bbox_min[k])) return fail(PO_ERR_INVALID_ARG, "bbox_min[%d] not finite", k);
     if (desc->max_depth < 1 || desc->max_depth > po::kMaxDepth)
         return fail(PO_ERR_INVALID_ARG, "max_depth %d outside [1,%d]", desc->max_depth, po::kMaxDepth);
-    if (desc->sh_degree < 0 || desc->sh_degree > 3)
-        return fail(PO_ERR_UNSUPPORTED, "sh_degree %d unsupported (0..3)", desc->sh_degree);
+    if (desc->sh_degree < 0 || desc->sh_degree > 4)
+        return fail(PO_ERR_UNSUPPORTED, "sh_degree %d unsupported (0..4)", desc->sh_degree);
     if (desc->payload != PO_F32 && desc->payload != PO_F16)
         return fail(PO_ERR_UNSUPPORTED, "payload %d unsupported", desc->payload);
     if (desc->sh_sign != PO_SH_CS && desc->sh_sign != PO_SH_NO_CS)

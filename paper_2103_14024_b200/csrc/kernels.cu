@@ -993,6 +993,8 @@ __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* _
         case 5: { constexpr int DEG = 2; constexpr bool F16 = true; __VA_ARGS__; } break;  \
         case 6: { constexpr int DEG = 3; constexpr bool F16 = false; __VA_ARGS__; } break; \
         case 7: { constexpr int DEG = 3; constexpr bool F16 = true; __VA_ARGS__; } break;  \
+        case 8: { constexpr int DEG = 4; constexpr bool F16 = false; __VA_ARGS__; } break; \
+        case 9: { constexpr int DEG = 4; constexpr bool F16 = true; __VA_ARGS__; } break;  \
         default: return cudaErrorInvalidValue;                         \
     }
 

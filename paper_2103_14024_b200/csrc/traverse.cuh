@@ -353,6 +353,18 @@ __device__ __forceinline__ void sh_basis(const float d[3], float odd, float* Y) 
             Y[13] = odd * 0.45704579946446572f * x * (5.f * zz - 1.f);
             Y[14] = 1.4453057213202769f * z * (xx - yy);
             Y[15] = odd * 0.59004358992664352f * x * (xx - 3.f * yy);
+            if (DEG >= 4) {   // l = 4 (SH-25, the paper's T&T setting P:587-588), same sign convention
+                const float x2y2 = xx - yy, z7m1 = 7.f * zz - 1.f, z7m3 = 7.f * zz - 3.f;
+                Y[16] = 2.5033429417967046f * x * y * x2y2;
+                Y[17] = odd * 1.7701307697799304f * y * z * (3.f * xx - yy);
+                Y[18] = 0.94617469575756008f * x * y * z7m1;
+                Y[19] = odd * 0.66904654355728917f * y * z * z7m3;
+                Y[20] = 0.10578554691520430f * (zz * (35.f * zz - 30.f) + 3.f);
+                Y[21] = odd * 0.66904654355728917f * x * z * z7m3;
+                Y[22] = 0.47308734787878004f * x2y2 * z7m1;
+                Y[23] = odd * 1.7701307697799304f * x * z * (xx - 3.f * yy);
+                Y[24] = 0.62583573544917614f * (xx * (xx - 3.f * yy) - yy * (3.f * xx - yy));
+            }
         }
     }
 }

@@ -75,7 +75,7 @@ def test_rejects_malformed_trees(po):
     st, msg = _create(po, [[L | 0] + [0] * 7], [1.0], np.full((1, 1, 3), np.inf), depth=1)
     assert st == 2 and "not finite" in msg
     # unsupported degree / bad depth
-    st, _ = _create(po, [[0] * 8], [], np.zeros((0, 25, 3)), depth=1, deg=4)
+    st, _ = _create(po, [[0] * 8], [], np.zeros((0, 36, 3)), depth=1, deg=5)
     assert st == 5
     st, _ = _create(po, [[0] * 8], [], np.zeros((0, 1, 3)), depth=0)
     assert st == 1

@@ -83,7 +83,7 @@ def test_c0_trace_bit_exact(env, c0_tree, gamma):
     assert np.array_equal(nodes[ok], ref["nodes_met"][ok])
 
 
-@pytest.mark.parametrize("seed,depth,deg", [(1, 4, 0), (2, 5, 1), (3, 6, 2), (4, 7, 3), (5, 3, 3)])
+@pytest.mark.parametrize("seed,depth,deg", [(1, 4, 0), (2, 5, 1), (3, 6, 2), (4, 7, 3), (5, 3, 3), (6, 6, 4)])
 def test_random_trees_render_rays(env, seed, depth, deg):
     po, om, torch = env
     t = gen.scene_random(seed, depth=depth, sh_degree=deg, sigma_scale=3.0)
@@ -169,9 +169,10 @@ def test_multi_view_batch_and_host_path(env, c0_tree):
         assert np.abs(dev[i].reshape(-1, 3)[ok] - ref["rgb"][ok]).max() <= RGB_TOL
 
 
-def test_sh_sign_convention(env):
+@pytest.mark.parametrize("deg", [3, 4])
+def test_sh_sign_convention(env, deg):
     po, om, torch = env
-    t = gen.scene_random(13, depth=3, sh_degree=3)
+    t = gen.scene_random(13, depth=3, sh_degree=deg)
     rays = gen.random_rays(14, 500)
     r64 = rays.astype(np.float64)
     for sign, cs in ((po.PO_SH_CS, 1), (po.PO_SH_NO_CS, 0)):
@@ -183,9 +184,10 @@ def test_sh_sign_convention(env):
         assert np.abs(out[ok] - ref["rgb"][ok]).max() <= RGB_TOL
 
 
-def test_fp16_payload(env):
+@pytest.mark.parametrize("deg", [3, 4])
+def test_fp16_payload(env, deg):
     po, om, torch = env
-    t = gen.scene_random(15, depth=6, sh_degree=3, sigma_scale=3.0)
+    t = gen.scene_random(15, depth=6, sh_degree=deg, sigma_scale=3.0)
     tree = po.tree_from_gen(t, payload=po.PO_F16)
     rays = gen.random_rays(16, 4000)
     r64 = rays.astype(np.float64)
@@ -348,7 +350,7 @@ def test_backward_plan_exact(env):
 
 
 @pytest.mark.parametrize("seed,deg,max_seg", [(31, 1, None), (32, 2, None), (33, 3, None), (34, 0, None),
-                                              (35, 3, 8), (36, 1, 8)])
+                                              (35, 3, 8), (36, 1, 8), (37, 4, None), (38, 4, 8)])
 def test_random_tree_backward(env, seed, deg, max_seg):
     po, om, torch = env
     t = gen.scene_random(seed, depth=5, sh_degree=deg)
@@ -420,7 +422,7 @@ def test_loss_grad_and_sgd(env):
         po.po_tree_sgd_step(tq, gs, gk, 0.25)
 
 
-@pytest.mark.parametrize("deg", [0, 1, 3])
+@pytest.mark.parametrize("deg", [0, 1, 3, 4])
 def test_sgd_range_sparse_and_zeroing(env, deg):
     """po_tree_sgd_step_range over ragged ranges (quad path + scalar head/tail, ne = 3 / 12 / 48):
     p -= lr g exactly where g != 0, untouched where g == 0, and PO_SGD_ZERO_GRAD zeroes exactly

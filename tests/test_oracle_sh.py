@@ -72,9 +72,9 @@ def test_scipy_complex_cross_check(oracle_mod):
     d = _unit(64, 4)
     theta = np.arccos(np.clip(d[:, 2], -1, 1))
     phi = np.arctan2(d[:, 1], d[:, 0])
-    Y = oracle_mod.sh_basis_n(3, d)
+    Y = oracle_mod.sh_basis_n(4, d)
     b = 0
-    for l in range(4):
+    for l in range(5):   # l = 4: SH-25, the paper's T&T setting
         for m in range(-l, l + 1):
             am = abs(m)
             Yc = sp.sph_harm_y(l, am, theta, phi)   # complex SH, Condon-Shortley phase included
@@ -109,6 +109,31 @@ def _textbook_table(d):
 def test_textbook_cartesian_table(oracle_mod):
     d = _unit(200, 5)
     np.testing.assert_allclose(oracle_mod.sh_basis_n(3, d), _textbook_table(d), atol=1e-12)
+
+
+def _textbook_l4(d):
+    """Cartesian real SH, l = 4, m = -4..4 (same sign-free convention)."""
+    x, y, z = d[:, 0], d[:, 1], d[:, 2]
+    pi = np.pi
+    c = [
+        0.75 * np.sqrt(35 / pi) * x * y * (x * x - y * y),
+        0.75 * np.sqrt(35 / (2 * pi)) * y * z * (3 * x * x - y * y),
+        0.75 * np.sqrt(5 / pi) * x * y * (7 * z * z - 1),
+        0.75 * np.sqrt(5 / (2 * pi)) * y * z * (7 * z * z - 3),
+        3 / 16 * np.sqrt(1 / pi) * (35 * z ** 4 - 30 * z * z + 3),
+        0.75 * np.sqrt(5 / (2 * pi)) * x * z * (7 * z * z - 3),
+        3 / 8 * np.sqrt(5 / pi) * (x * x - y * y) * (7 * z * z - 1),
+        0.75 * np.sqrt(35 / (2 * pi)) * x * z * (x * x - 3 * y * y),
+        3 / 16 * np.sqrt(35 / pi) * (x * x * (x * x - 3 * y * y) - y * y * (3 * x * x - y * y)),
+    ]
+    return np.stack(c, -1)
+
+
+def test_textbook_cartesian_table_l4(oracle_mod):
+    d = _unit(200, 7)
+    np.testing.assert_allclose(oracle_mod.sh_basis_n(4, d)[:, 16:], _textbook_l4(d), atol=1e-12)
+    # addition theorem for l = 4: sum_m Y_4^m(d)^2 = 9 / (4 pi) for every direction
+    np.testing.assert_allclose((oracle_mod.sh_basis_n(4, d)[:, 16:] ** 2).sum(1), 9 / (4 * np.pi), atol=1e-12)
 
 
 def test_no_cs_convention_flips_odd_m(oracle_mod):
