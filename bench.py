@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 W = H = 800
 GAMMA = 0.01
 METRIC = "800x800 FPS, SH-3 512^3 PlenOctree (c1)"
+C2_VIEWS = 200
 UNIT = "frames/s"
 L2_FLUSH_BYTES = 256 << 20
 
@@ -123,7 +124,14 @@ def _init_pg(dev_index: int):
         dist.init_process_group(backend)
 
 
-def _workload_desc(tree_gen, wl="c1"):
+def _workload_desc(tree_gen, wl="c1", ws=1):
+    if wl == "c2":
+        return {"workload": "c2: the c1 tree (depth-9, "
+                            f"{tree_gen.n_leaves} leaves, SH-3 fp32), a 200-view 800x800 orbit per step, gamma 0.01",
+                "views": "az = 1.8*i deg, el 30 deg, r 3.4, f 1111.1 px, i = 0..199; rank r renders views "
+                         f"i = r (mod {ws}) in ONE launch",
+                "l2": "flushed (256 MiB write) before every timed step; only the render is inside the CUDA events",
+                "global_batch": "200 views per step (all ranks)"}
     if wl == "c3":
         return {"workload": "c3: Tanks&Temples-shaped bounded scene, depth-10 sparse octree (1024^3), "
                             f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp16 payload (sigma fp32), "
@@ -147,7 +155,9 @@ def run_ours(args):
     wl = args.workload
     W, H = (1920, 1080) if wl == "c3" else (800, 800)
     payload = po.PO_F16 if wl == "c3" else po.PO_F32
-    metric = "1920x1080 FPS, SH-3 depth-10 fp16 PlenOctree (c3)" if wl == "c3" else METRIC
+    metric = {"c3": "1920x1080 FPS, SH-3 depth-10 fp16 PlenOctree (c3)",
+              "c2": "views/s, 200-view 800x800 orbit, SH-3 512^3 PlenOctree (c2)"}.get(wl, METRIC)
+    unit = "views/s" if wl == "c2" else UNIT
     ws, rank, local = _dist()
     if ws > 1:
         _init_pg(local)
@@ -156,27 +166,35 @@ def run_ours(args):
     po.lib()
     t_gen = gen.scene_c3() if wl == "c3" else gen.scene_c1()
     tree = po.tree_from_gen(t_gen, payload=payload, device=local)
-    V = max(1, args.views_per_launch)
-    n_views = max(args.steps + args.warmup, 1) * ws * V
-    cam_recs = np.concatenate([gen.config_camera(wl, v)[0] for v in range(n_views)])
+    if wl == "c2":
+        # every step renders the whole 200-view orbit: rank r takes views r, r+N, ... in one launch
+        mine = list(range(rank, C2_VIEWS, ws))
+        V = len(mine)
+        cam_recs = np.concatenate([gen.config_camera("c2", v)[0] for v in mine])
+        n_views = V
+    else:
+        V = max(1, args.views_per_launch)
+        n_views = max(args.steps + args.warmup, 1) * ws * V
+        cam_recs = np.concatenate([gen.config_camera(wl, v)[0] for v in range(n_views)])
     cams = po.cams_tensor(cam_recs, dev)
     out = torch.empty((V, H, W, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def view_of(step):   # first of the V consecutive orbit views rank `rank` renders at `step`
-        return ((step * ws + rank) * V) % n_views
+    def view_of(step):   # first of the V consecutive views rank `rank` renders at `step`
+        return 0 if wl == "c2" else ((step * ws + rank) * V) % n_views
 
     # algorithmic bytes per launch: counters of the same traversal
     B = t_gen.basis_dim
     row_bytes = 3 * B * (2 if payload == po.PO_F16 else 4)
     stats = {"leaf_visits": 0, "sh_rows": 0, "nodes": 0, "hit_rays": 0, "boxes": 0, "leaf_level_boxes": 0,
              "warp_boxes": 0}
-    for s in range(args.warmup, args.warmup + args.steps):
+    stat_steps = range(args.warmup, args.warmup + (1 if wl == "c2" else args.steps))
+    for s in stat_steps:
         v = view_of(s)
         st = po.po_render_stats(tree, cams[v:v + V], W, H, gamma=GAMMA)
         for k in stats:
-            stats[k] += st[k]
+            stats[k] += st[k] * (args.steps if wl == "c2" else 1)   # c2: every step renders the same orbit
     K = max(args.steps, 1)
     alg_bytes = ((stats["leaf_visits"] * 4 + stats["sh_rows"] * row_bytes + stats["nodes"] * 32) / K
                  + (W * H * 12 + 64) * V)
@@ -215,7 +233,7 @@ def run_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_per_step = t_max / K
-    fps = ws * K * V / (t_max / 1e3)
+    fps = (C2_VIEWS if wl == "c2" else ws * V) * K / (t_max / 1e3)
     kernel_ms = t_ms / K   # one kernel launch per step
 
     # e2e: the same frames through the host-buffer C-ABI entry point (H2D cameras, D2H image)
@@ -223,7 +241,7 @@ def run_ours(args):
     cams_pinned = torch.empty((n_views, 16), dtype=torch.float32, pin_memory=True).numpy()
     cams_pinned[:] = np.frombuffer(np.ascontiguousarray(cam_recs).tobytes(), dtype=np.float32).reshape(-1, 16)
     e2e_ms = 0.0
-    e2e_steps = min(K, 50)
+    e2e_steps = min(K, 3 if wl == "c2" else 50)
     for s in range(2):
         po.po_render_host(tree, cams_pinned[view_of(s):view_of(s) + V], W, H, out_host=pinned, gamma=GAMMA)
     if ws > 1:
@@ -242,23 +260,27 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_fps = ws * e2e_steps * V / (e2e_ms / 1e3)
+    e2e_fps = (C2_VIEWS if wl == "c2" else ws * V) * e2e_steps / (e2e_ms / 1e3)
 
     if rank == 0:
         peak, peak_src = _peaks()
         achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
         traffic, tsrc = _ncu_traffic() if wl == "c1" else (None, None)
         line = {
-            "metric": metric, "value": round(fps, 2), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": metric, "value": round(fps, 2), "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural SDF scene, seeded)",
-            "config": _workload_desc(t_gen, wl) | {"parallelism": f"view-sharded x{ws}, tree replicated"}
-                      | ({"global_batch": f"{V} frames per rank per step (one launch)"} if V > 1 else {})
+            "scaling": "strong" if wl == "c2" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (procedural SDF scene, seeded)",
+            "config": _workload_desc(t_gen, wl, ws) | {"parallelism": f"view-sharded x{ws}, tree replicated"}
+                      | ({"global_batch": f"{V} frames per rank per step (one launch)"} if V > 1 and wl != "c2"
+                         else {})
                       | ({"l2": f"NOT flushed ({args.l2}): analysis only"} if args.l2 != "flush" else {}),
             "mrays_per_s": round(fps * W * H / 1e6, 1),
-            "leaf_visits_per_frame": stats["leaf_visits"] / K,
-            "traversal_per_frame": {"boxes": stats["boxes"] / K, "leaf_level_boxes": stats["leaf_level_boxes"] / K,
-                                    "internal_nodes_met": stats["nodes"] / K, "hit_rays": stats["hit_rays"] / K,
+            "leaf_visits_per_frame": stats["leaf_visits"] / (K * V),
+            "traversal_per_frame": {"boxes": stats["boxes"] / (K * V),
+                                    "leaf_level_boxes": stats["leaf_level_boxes"] / (K * V),
+                                    "internal_nodes_met": stats["nodes"] / (K * V),
+                                    "hit_rays": stats["hit_rays"] / (K * V),
                                     "simt_step_efficiency": round(stats["boxes"] / max(1, 32 * stats["warp_boxes"]),
                                                                   4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -268,7 +290,7 @@ def run_ours(args):
                          "alg_bytes_def": f"leaf visits*4 B sigma + SH rows*{row_bytes} B + internal nodes met*32 B "
                                           "+ 12 B/pixel out",
                          "traffic_source": tsrc},
-            "e2e": {"value": round(e2e_fps, 2), "unit": UNIT, "h2d_bytes_per_step": 64 * V,
+            "e2e": {"value": round(e2e_fps, 2), "unit": unit, "h2d_bytes_per_step": 64 * V,
                     "d2h_bytes_per_step": W * H * 12 * V, "entry": "po_render_host (host cameras -> host image)"},
             "gpu_launches": int(launches),
             "clocks": clk,
@@ -472,7 +494,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c1", "c3", "c4"], default="c1")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4"], default="c1")
     ap.add_argument("--views-per-launch", type=int, default=1,
                     help="render V consecutive orbit views per po_render launch (c2-style batches)")
     ap.add_argument("--l2", choices=["flush", "orbit", "same"], default="flush",
