@@ -701,6 +701,7 @@ po_status po_render_backward_chunk(const po_tree* t, const float* rays, const in
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     po_tree* mt = const_cast<po_tree*>(t);   // work counters only
+    if (segments != nullptr && aux != nullptr) g_launches.fetch_add(1);   // + the replay kernel
     return launched(po::launch_backward_chunk(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, perm,
                                               chunk_ray_end, chunk, dL_dC, aux, sg, o, grad_sigma, grad_sh,
                                               mt->work_of(mt->next_slot()), (cudaStream_t)stream),
@@ -721,6 +722,7 @@ po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, con
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    if (segments != nullptr && aux != nullptr) g_launches.fetch_add(1);   // replay + overflow re-traversal
     return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
                                         sg, o, grad_sigma, grad_sh, (cudaStream_t)stream),
                     "po_render_backward");

@@ -667,16 +667,13 @@ __global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __
 // then every lane applies GradVisitor::seg's formula to its own segment.  Rays whose segments
 // overflowed (count > max_seg) are left to k_backward<..., true>.
 template <int DEG>
-__global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const float* __restrict__ rays, int64_t n,
-                                                         const float* __restrict__ dL_dC,
-                                                         const double* __restrict__ aux, SegIn si,
-                                                         float* __restrict__ grad_sigma,
-                                                         float* __restrict__ grad_sh) {
+__device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __restrict__ rays, int64_t i,
+                                           const float* __restrict__ dL_dC, const double* __restrict__ aux,
+                                           const SegIn& si, float* __restrict__ grad_sigma,
+                                           float* __restrict__ grad_sh) {
     constexpr int B = ShDim<DEG>::B;
     constexpr int NE = 3 * B;
     const int lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= n) return;
     const int32_t ns = __ldg(si.count + i);
     if (ns == 0 || ns > si.max_seg) return;
     float g[3], dir[3], d[3];
@@ -741,12 +738,41 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const fl
     }
 }
 
+template <int DEG>
+__global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                         const float* __restrict__ dL_dC,
+                                                         const double* __restrict__ aux, SegIn si,
+                                                         float* __restrict__ grad_sigma,
+                                                         float* __restrict__ grad_sh) {
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= n) return;
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, grad_sigma, grad_sh);
+}
+
+// the same over one chunk of a po_backward_plan (bounds on the device): a persistent grid
+// whose warps stride over perm[chunk_end[c-1] .. chunk_end[c]) (static: ~100 rays per warp on
+// c4, balanced without a shared counter)
+template <int DEG>
+__global__ void __launch_bounds__(256, 3) k_backward_replay_chunk(DevTree tr, const float* __restrict__ rays,
+                                                               const int32_t* __restrict__ perm,
+                                                               const int64_t* __restrict__ chunk_end, int chunk,
+                                                               const float* __restrict__ dL_dC,
+                                                               const double* __restrict__ aux, SegIn si,
+                                                               float* __restrict__ grad_sigma,
+                                                               float* __restrict__ grad_sh) {
+    const int64_t b = chunk > 0 ? chunk_end[chunk - 1] : 0, e = chunk_end[chunk];
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = b + w0; j < e; j += nw)
+        replay_ray<DEG>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, grad_sigma, grad_sh);
+}
+
 // Pass 2 over one chunk of a po_backward_plan: rays perm[chunk_end[c-1] .. chunk_end[c]).
 // The bounds live on the device (no host sync between the plan and the chunks), so the grid
 // is persistent and warps claim 32-ray batches from a global counter (work[0]); no warp waits
 // for a slower one (CTA-wide 256-ray claims measured 5 % slower at K = 2 and 4); the last CTA
 // resets the counters (work[1] = finished CTAs) for the next launch on the stream.
-template <int DEG, bool F16>
+template <int DEG, bool F16, bool kSkipReplay>
 __global__ void __launch_bounds__(256, 2) k_backward_chunk(DevTree tr, const float* __restrict__ rays,
                                                         const int32_t* __restrict__ perm,
                                                         const int64_t* __restrict__ chunk_end, int chunk,
@@ -765,7 +791,8 @@ __global__ void __launch_bounds__(256, 2) k_backward_chunk(DevTree tr, const flo
         if ((int64_t)k >= nb) break;
         const int64_t j = b + ((int64_t)k << 5) + lane;
         if (j < e)
-            backward_ray<DEG, F16>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, opt, grad_sigma, grad_sh, stk);
+            backward_ray<DEG, F16, kSkipReplay>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, opt, grad_sigma,
+                                                grad_sh, stk);
         __syncwarp();
     }
     __syncthreads();
@@ -1133,10 +1160,20 @@ cudaError_t launch_backward_chunk(const DevTree& tr, int deg, bool f16, const fl
                                   const Segments& sg, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
                                   unsigned* work, cudaStream_t s) {
     const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+    const bool replay = aux != nullptr && sg.count != nullptr;
     PO_DISPATCH(deg, f16, {
-        static const int grid = persistent_grid(k_backward_chunk<DEG, F16>, 1 << 30, 0);
-        k_backward_chunk<DEG, F16><<<grid, 256, 0, s>>>(tr, rays, perm, chunk_end, chunk, dL_dC, aux, si, opt,
-                                                        grad_sigma, grad_sh, work);
+        if (replay) {   // stored segments warp-per-ray, then the chunk's overflow rays by re-traversal
+            static const int rgrid = persistent_grid(k_backward_replay_chunk<DEG>, 1 << 30, 0);
+            k_backward_replay_chunk<DEG><<<rgrid, 256, 0, s>>>(tr, rays, perm, chunk_end, chunk, dL_dC, aux, si,
+                                                               grad_sigma, grad_sh);
+            static const int grid = persistent_grid(k_backward_chunk<DEG, F16, true>, 1 << 30, 0);
+            k_backward_chunk<DEG, F16, true><<<grid, 256, 0, s>>>(tr, rays, perm, chunk_end, chunk, dL_dC, aux, si,
+                                                                  opt, grad_sigma, grad_sh, work);
+        } else {
+            static const int grid = persistent_grid(k_backward_chunk<DEG, F16, false>, 1 << 30, 0);
+            k_backward_chunk<DEG, F16, false><<<grid, 256, 0, s>>>(tr, rays, perm, chunk_end, chunk, dL_dC, aux, si,
+                                                                   opt, grad_sigma, grad_sh, work);
+        }
     });
     return cudaGetLastError();
 }
