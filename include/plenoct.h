@@ -84,6 +84,17 @@ const char* po_version(void);
  * po_tree_destroy. */
 po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_t n_nodes, const float* sigma,
                          const float* sh, int64_t n_leaves, po_tree** out);
+/* Overwrite every leaf's sigma~ and SH coefficients from host arrays laid out as in
+ * po_tree_create (fp16 payloads round to nearest-even); the structure is unchanged.  Waits for
+ * the device first; PO_ERR_INVALID_ARG on a non-finite value (nothing written then).  With
+ * po_tree_read_leaves this snapshots / restores a tree during optimisation (early stopping). */
+po_status po_tree_write_leaves(po_tree* tree, const float* sigma, const float* sh);
+
+/* Export (NEXT f2; "the entire optimization process is done in float32 ... after it we
+ * store the PlenOctree with float16"): a new tree with the same structure and leaf values
+ * re-uploaded with `payload` (PO_F16: SH coefficients rounded to nearest-even, sigma~ stays
+ * fp32, reading Q20).  Synchronous; src is unchanged and independent of *out. */
+po_status po_tree_convert(const po_tree* src, int32_t payload, po_tree** out);
 po_status po_tree_destroy(po_tree* tree);
 /* sh_row_bytes: padded device row of one leaf's SH payload (16-byte multiple). */
 po_status po_tree_info(const po_tree* tree, int64_t* n_nodes, int64_t* n_leaves, int32_t* sh_row_bytes);

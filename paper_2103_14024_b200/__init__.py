@@ -23,7 +23,8 @@ PO_SH_CS, PO_SH_NO_CS = 0, 1
 STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_ERR_OOM", 4: "PO_ERR_CUDA",
           5: "PO_ERR_UNSUPPORTED"}
 
-EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_destroy", "po_tree_info",
+EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
+           "po_tree_info", "po_tree_write_leaves",
            "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_backward_plan", "po_render_backward_chunk",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
@@ -86,6 +87,8 @@ def lib():
         L.po_launch_count.restype = I64
         L.po_tree_create.argtypes = [P, P, I64, P, P, I64, ctypes.POINTER(P)]
         L.po_tree_destroy.argtypes = [P]
+        L.po_tree_convert.argtypes = [P, I32, ctypes.POINTER(P)]
+        L.po_tree_write_leaves.argtypes = [P, P, P]
         L.po_tree_info.argtypes = [P, P, P, P]
         L.po_tree_read_leaves.argtypes = [P, P, P]
         L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
@@ -180,6 +183,11 @@ class PlenOctree:
         _check(lib().po_tree_read_leaves(self.handle, _ptr(sig), _ptr(sh)))
         return sig, sh
 
+    def write_leaves(self, sigma, sh):
+        sigma = np.ascontiguousarray(sigma, dtype=np.float32).reshape(self.n_leaves)
+        sh = np.ascontiguousarray(sh, dtype=np.float32).reshape(self.n_leaves, self.B, 3)
+        _check(lib().po_tree_write_leaves(self.handle, _ptr(sigma), _ptr(sh)))
+
     def destroy(self):
         if self._h is not None:
             lib().po_tree_destroy(self._h)
@@ -205,6 +213,15 @@ def po_tree_create(child, sigma, sh, depth: int, sh_degree: int, bbox_min=(-1.0,
     _check(lib().po_tree_create(ctypes.byref(desc), _ptr(child), child.shape[0], _ptr(sigma), _ptr(sh),
                                 sigma.shape[0], ctypes.byref(h)))
     return PlenOctree(h, desc, child.shape[0], sigma.shape[0])
+
+
+def po_tree_convert(tree: PlenOctree, payload: int = PO_F16) -> PlenOctree:
+    """Export a (trained, fp32) tree with another payload, e.g. fp16."""
+    h = ctypes.c_void_p()
+    _check(lib().po_tree_convert(tree.handle, int(payload), ctypes.byref(h)))
+    desc = TreeDesc.from_buffer_copy(tree.desc)
+    desc.payload = int(payload)
+    return PlenOctree(h, desc, tree.n_nodes, tree.n_leaves)
 
 
 def tree_from_gen(tree, payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0) -> PlenOctree:

@@ -50,6 +50,7 @@ struct po_tree {
     std::atomic<uint32_t> work_rr{0};
     int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
     unsigned* work_of(int slot) { return d_work + 2 * slot; }
+    std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
     // po_backward_plan scratch (sort keys/values + CUB temp), grown on demand
     void* d_plan = nullptr;
     size_t plan_cap = 0;
@@ -431,8 +432,49 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
             if (e != cudaSuccess) return cleanup(cuda_status(e, "upload sh"));
         }
     }
+    t->h_child.assign(child, child + (size_t)n_nodes * 8);
     *out = t;
     return PO_OK;
+}
+
+po_status po_tree_write_leaves(po_tree* t, const float* sigma, const float* sh) {
+    if (po_status s = check_tree(t)) return s;
+    if (t->n_leaves == 0) return PO_OK;
+    if (!sigma || !sh) return fail(PO_ERR_INVALID_ARG, "sigma / sh NULL");
+    for (int64_t i = 0; i < t->n_leaves; ++i) {
+        if (!std::isfinite(sigma[i])) return fail(PO_ERR_INVALID_ARG, "sigma of leaf %lld not finite", (long long)i);
+        for (int j = 0; j < t->ne; ++j)
+            if (!std::isfinite(sh[i * t->ne + j]))
+                return fail(PO_ERR_INVALID_ARG, "sh of leaf %lld not finite", (long long)i);
+    }
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaError_t e = cudaDeviceSynchronize();   // stream-ordered writers of the tree finish first
+    if (e != cudaSuccess) return cuda_status(e, "sync");
+    if ((e = cudaMemcpy(t->d_sigma, sigma, (size_t)t->n_leaves * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_status(e, "write sigma");
+    const bool f16 = t->desc.payload == PO_F16;
+    const size_t elt = f16 ? 2 : 4;
+    std::vector<uint8_t> buf((size_t)t->n_leaves * t->sh_row * elt, 0);
+    for (int64_t i = 0; i < t->n_leaves; ++i)
+        for (int j = 0; j < t->ne; ++j) {
+            if (f16) reinterpret_cast<__half*>(buf.data())[i * t->sh_row + j] = __float2half_rn(sh[i * t->ne + j]);
+            else reinterpret_cast<float*>(buf.data())[i * t->sh_row + j] = sh[i * t->ne + j];
+        }
+    if ((e = cudaMemcpy(t->d_sh, buf.data(), buf.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_status(e, "write sh");
+    return PO_OK;
+}
+
+po_status po_tree_convert(const po_tree* src, int32_t payload, po_tree** out) {
+    if (!out) return fail(PO_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (po_status s = check_tree(src)) return s;
+    std::vector<float> sigma((size_t)src->n_leaves), sh((size_t)src->n_leaves * src->ne);
+    if (po_status s = po_tree_read_leaves(src, sigma.data(), sh.data())) return s;
+    po_tree_desc d = src->desc;
+    d.payload = payload;
+    return po_tree_create(&d, src->h_child.data(), src->n_nodes, sigma.data(), sh.data(), src->n_leaves, out);
 }
 
 po_status po_tree_destroy(po_tree* t) {
