@@ -37,7 +37,8 @@ class OrTree(ctypes.Structure):
                 ("sh", ctypes.c_void_p), ("sh32", ctypes.c_void_p), ("n_leaves", ctypes.c_int64),
                 ("depth", ctypes.c_int32),
                 ("sh_degree", ctypes.c_int32), ("sh_cs", ctypes.c_int32), ("pad_", ctypes.c_int32),
-                ("bbox_min", ctypes.c_double * 3), ("edge", ctypes.c_double)]
+                ("bbox_min", ctypes.c_double * 3), ("edge", ctypes.c_double),
+                ("sg_axes", ctypes.c_void_p), ("sg_lambda", ctypes.c_void_p)]
 
 
 def lib():
@@ -56,6 +57,7 @@ def lib():
         _lib.or_tie_flags.argtypes = [P, P, I64, D, D, D, P, ctypes.c_int]
         _lib.or_render_depth.argtypes = [P, P, I64, D, P, P, ctypes.c_int]
         _lib.or_leaf_max_alpha.argtypes = [P, P, I64, D, P, ctypes.c_int]
+        _lib.or_sg_basis.argtypes = [ctypes.c_int, P, P, I64, P, P]
     return _lib
 
 
@@ -66,7 +68,8 @@ def _ptr(a):
 class OracleTree:
     """Holds contiguous copies of the host arrays and the or_tree descriptor."""
 
-    def __init__(self, tree, sh_cs: int = 1, sigma=None, sh=None):
+    def __init__(self, tree, sh_cs: int = 1, sigma=None, sh=None, sg=None):
+        """sg: optional (axes [B][3], lambda [B]) -> spherical-Gaussian basis (NEXT f3)."""
         self.child = np.ascontiguousarray(tree.child, dtype=np.uint32)
         # sigma widened exactly to float64; SH kept as given: float64 arrays (finite-difference
         # tests) are used directly, fp32 / fp16 ones are stored as fp32 and widened exactly in C
@@ -82,7 +85,13 @@ class OracleTree:
                            _ptr(self.sh).value if self.sh is not None else None,
                            _ptr(self.sh32).value if self.sh32 is not None else None,
                            self.n_leaves, tree.depth, tree.sh_degree, sh_cs, 0,
-                           (ctypes.c_double * 3)(*[float(v) for v in tree.bbox_min]), float(tree.edge))
+                           (ctypes.c_double * 3)(*[float(v) for v in tree.bbox_min]), float(tree.edge),
+                           None, None)
+        if sg is not None:
+            self.sg_axes = np.ascontiguousarray(sg[0], dtype=np.float64).reshape(self.B, 3)
+            self.sg_lambda = np.ascontiguousarray(sg[1], dtype=np.float64).reshape(self.B)
+            self.desc.sg_axes = _ptr(self.sg_axes).value
+            self.desc.sg_lambda = _ptr(self.sg_lambda).value
 
     @property
     def ref(self):
@@ -94,6 +103,16 @@ def sh_basis(lmax: int, d, cs: int = 1) -> np.ndarray:
     Y = np.zeros((lmax + 1) ** 2)
     assert lib().or_sh_basis(lmax, cs, _ptr(d), _ptr(Y)) == 0
     return Y
+
+
+def sg_basis_n(axes, lam, dirs) -> np.ndarray:
+    """Spherical Gaussians G_b(d) = exp(lambda_b (d . p_b - 1)) for dirs [n][3]."""
+    axes = np.ascontiguousarray(axes, dtype=np.float64).reshape(-1, 3)
+    lam = np.ascontiguousarray(lam, dtype=np.float64).reshape(-1)
+    dirs = np.ascontiguousarray(dirs, dtype=np.float64).reshape(-1, 3)
+    G = np.zeros((dirs.shape[0], axes.shape[0]))
+    assert lib().or_sg_basis(axes.shape[0], _ptr(axes), _ptr(lam), dirs.shape[0], _ptr(dirs), _ptr(G)) == 0
+    return G
 
 
 def sh_basis_n(lmax: int, dirs, cs: int = 1) -> np.ndarray:

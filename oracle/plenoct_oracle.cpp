@@ -48,6 +48,10 @@ typedef struct {
     int32_t pad_;
     double bbox_min[3];
     double edge;
+    // NEXT f3, spherical Gaussians: when sg_axes != NULL the B = (sh_degree+1)^2
+    // per-channel basis functions are G_b(d) = exp(lambda_b (d . p_b - 1)) instead of SH
+    const double* sg_axes;     // [B][3] lobe axes p_b (normalised here, reading Q36)
+    const double* sg_lambda;   // [B] bandwidths lambda_b
 } or_tree;
 
 }  // extern "C"
@@ -254,6 +258,26 @@ void segments(const or_tree* T, const Ray& r, int mode, const std::vector<LeafBo
 inline double sigmoid(double z) { return 1.0 / (1.0 + std::exp(-z)); }
 
 // Eq. (5): c_ch = S(sum_b k_{b,ch} Y_b)
+// Spherical Gaussian basis: G(d; p, lambda) = e^{lambda (d . p - 1)}, p a unit axis.
+void sg_basis(int B, const double* axes, const double* lambda, const double* dir, double* G) {
+    for (int b = 0; b < B; ++b) {
+        const double* p = axes + 3 * b;
+        double n = std::sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+        double dp = (dir[0] * p[0] + dir[1] * p[1] + dir[2] * p[2]) / n;
+        G[b] = std::exp(lambda[b] * (dp - 1.0));
+    }
+}
+
+// the per-ray basis of the tree: SH (App. B.1) or SG
+void ray_basis(const or_tree* T, const double* dir, double* Y) {
+    if (T->sg_axes) {
+        const int B = (T->sh_degree + 1) * (T->sh_degree + 1);
+        sg_basis(B, T->sg_axes, T->sg_lambda, dir, Y);
+    } else {
+        sh_basis(T->sh_degree, T->sh_cs, dir, Y);
+    }
+}
+
 inline void leaf_color(const or_tree* T, int64_t leaf, const double* Y, int B, double c[3]) {
     const int64_t off = leaf * (int64_t)B * 3;
     for (int ch = 0; ch < 3; ++ch) {
@@ -323,6 +347,12 @@ extern "C" {
 int or_sh_basis(int lmax, int cs, const double* dir, double* Y) {
     if (lmax < 0 || lmax > 10) return 1;
     sh_basis(lmax, cs, dir, Y);
+    return 0;
+}
+
+int or_sg_basis(int B, const double* axes, const double* lambda, int64_t n, const double* dirs, double* G) {
+    if (B < 1) return 1;
+    for (int64_t i = 0; i < n; ++i) sg_basis(B, axes, lambda, dirs + i * 3, G + i * B);
     return 0;
 }
 
@@ -402,7 +432,7 @@ int or_render(const or_tree* T, const double* rays, int64_t n, double gamma, con
             double tn, tf;
             bool hit;
             segments(T, r, mode, &boxes, cx, &tn, &tf, &hit);
-            sh_basis(T->sh_degree, T->sh_cs, r.d, Y.data());
+            ray_basis(T, r.d, Y.data());
             Comp c = composite(T, cx.segs, Y.data(), B, gamma, bg);
             for (int ch = 0; ch < 3; ++ch) rgb[i * 3 + ch] = c.rgb[ch];
             if (T_final) T_final[i] = c.T;
@@ -444,7 +474,7 @@ int or_backward(const or_tree* T, const double* rays, int64_t n, double gamma, c
             bool hit;
             segments(T, r, 0, nullptr, cx, &tn, &tf, &hit);
             if (!hit) continue;
-            sh_basis(T->sh_degree, T->sh_cs, r.d, Y.data());
+            ray_basis(T, r.d, Y.data());
             // forward quantities up to termination: M processed segments, T_0..T_M
             Ti.assign(1, 1.0);
             w.clear();
