@@ -84,6 +84,15 @@ const char* po_version(void);
  * po_tree_destroy. */
 po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_t n_nodes, const float* sigma,
                          const float* sh, int64_t n_leaves, po_tree** out);
+/* NEXT f3, spherical Gaussians (SG-25 with a tree of sh_degree 4): replace the
+ * tree's per-ray basis by B = (sh_degree+1)^2 lobes G_b(d) = exp(lambda_b (d . p_b - 1)); the
+ * leaf rows then hold one RGB coefficient per lobe (same layout), and render, backward (dL/dk
+ * uses G_b for Y_b) and every other kernel use them.  axes host float[B][3] (normalised here,
+ * reading Q36), lambda host float[B]; axes == NULL restores the SH basis.  The lobes are fixed
+ * (the paper learns them in NeRF-SG, before conversion).  Waits for the device first;
+ * PO_ERR_INVALID_ARG for a zero / non-finite axis or a non-finite bandwidth. */
+po_status po_tree_set_sg_basis(po_tree* tree, const float* axes, const float* lambda);
+
 /* Overwrite every leaf's sigma~ and SH coefficients from host arrays laid out as in
  * po_tree_create (fp16 payloads round to nearest-even); the structure is unchanged.  Waits for
  * the device first; PO_ERR_INVALID_ARG on a non-finite value (nothing written then).  With

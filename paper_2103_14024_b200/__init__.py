@@ -24,7 +24,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
           5: "PO_ERR_UNSUPPORTED"}
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
-           "po_tree_info", "po_tree_write_leaves",
+           "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis",
            "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_backward_plan", "po_render_backward_chunk",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
@@ -89,6 +89,7 @@ def lib():
         L.po_tree_destroy.argtypes = [P]
         L.po_tree_convert.argtypes = [P, I32, ctypes.POINTER(P)]
         L.po_tree_write_leaves.argtypes = [P, P, P]
+        L.po_tree_set_sg_basis.argtypes = [P, P, P]
         L.po_tree_info.argtypes = [P, P, P, P]
         L.po_tree_read_leaves.argtypes = [P, P, P]
         L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
@@ -187,6 +188,15 @@ class PlenOctree:
         sigma = np.ascontiguousarray(sigma, dtype=np.float32).reshape(self.n_leaves)
         sh = np.ascontiguousarray(sh, dtype=np.float32).reshape(self.n_leaves, self.B, 3)
         _check(lib().po_tree_write_leaves(self.handle, _ptr(sigma), _ptr(sh)))
+
+    def set_sg_basis(self, axes=None, lam=None):
+        """Spherical-Gaussian basis (B lobes: axes [B][3], bandwidths [B]); None restores SH."""
+        if axes is None:
+            _check(lib().po_tree_set_sg_basis(self.handle, None, None))
+            return
+        axes = np.ascontiguousarray(axes, dtype=np.float32).reshape(self.B, 3)
+        lam = np.ascontiguousarray(lam, dtype=np.float32).reshape(self.B)
+        _check(lib().po_tree_set_sg_basis(self.handle, _ptr(axes), _ptr(lam)))
 
     def destroy(self):
         if self._h is not None:

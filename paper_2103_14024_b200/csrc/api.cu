@@ -51,6 +51,8 @@ struct po_tree {
     int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
     unsigned* work_of(int slot) { return d_work + 2 * slot; }
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
+    float4* d_sg = nullptr;          // spherical-Gaussian lobes (po_tree_set_sg_basis) or null
+    std::vector<float> h_sg;         // the same on the host, [B][4]
     // po_backward_plan scratch (sort keys/values + CUB temp), grown on demand
     void* d_plan = nullptr;
     size_t plan_cap = 0;
@@ -146,6 +148,7 @@ po::DevTree dev_tree(const po_tree* t) {
     d.macro = t->d_macro;
     d.macro_shift = t->desc.max_depth - t->macro_level;
     d.macro_n = 1 << t->macro_level;
+    d.sg = t->d_sg;
     return d;
 }
 
@@ -437,6 +440,39 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     return PO_OK;
 }
 
+po_status po_tree_set_sg_basis(po_tree* t, const float* axes, const float* lambda) {
+    if (po_status s = check_tree(t)) return s;
+    const int B = t->B;
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaError_t e = cudaDeviceSynchronize();   // no render may be reading the old basis
+    if (e != cudaSuccess) return cuda_status(e, "sync");
+    if (!axes) {   // back to spherical harmonics
+        if (t->d_sg) cudaFree(t->d_sg);
+        t->d_sg = nullptr;
+        t->h_sg.clear();
+        return PO_OK;
+    }
+    if (!lambda) return fail(PO_ERR_INVALID_ARG, "lambda NULL");
+    std::vector<float> h((size_t)B * 4);
+    for (int b = 0; b < B; ++b) {
+        const double x = axes[3 * b], y = axes[3 * b + 1], z = axes[3 * b + 2];
+        const double n = std::sqrt(x * x + y * y + z * z);
+        if (!(n > 0.0) || !std::isfinite(n) || !std::isfinite(lambda[b]))
+            return fail(PO_ERR_INVALID_ARG, "lobe %d: zero / non-finite axis or bandwidth", b);
+        h[4 * b] = (float)(x / n);
+        h[4 * b + 1] = (float)(y / n);
+        h[4 * b + 2] = (float)(z / n);
+        h[4 * b + 3] = lambda[b];
+    }
+    if (!t->d_sg && (e = cudaMalloc(&t->d_sg, sizeof(float4) * B)) != cudaSuccess)
+        return cuda_status(e, "cudaMalloc(sg)");
+    if ((e = cudaMemcpy(t->d_sg, h.data(), sizeof(float4) * B, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_status(e, "upload sg");
+    t->h_sg = h;
+    return PO_OK;
+}
+
 po_status po_tree_write_leaves(po_tree* t, const float* sigma, const float* sh) {
     if (po_status s = check_tree(t)) return s;
     if (t->n_leaves == 0) return PO_OK;
@@ -474,7 +510,20 @@ po_status po_tree_convert(const po_tree* src, int32_t payload, po_tree** out) {
     if (po_status s = po_tree_read_leaves(src, sigma.data(), sh.data())) return s;
     po_tree_desc d = src->desc;
     d.payload = payload;
-    return po_tree_create(&d, src->h_child.data(), src->n_nodes, sigma.data(), sh.data(), src->n_leaves, out);
+    po_status st = po_tree_create(&d, src->h_child.data(), src->n_nodes, sigma.data(), sh.data(), src->n_leaves, out);
+    if (st == PO_OK && !src->h_sg.empty()) {   // keep a spherical-Gaussian basis
+        std::vector<float> ax((size_t)src->B * 3), lam((size_t)src->B);
+        for (int b = 0; b < src->B; ++b) {
+            for (int k = 0; k < 3; ++k) ax[3 * b + k] = src->h_sg[4 * b + k];
+            lam[b] = src->h_sg[4 * b + 3];
+        }
+        st = po_tree_set_sg_basis(*out, ax.data(), lam.data());
+        if (st != PO_OK) {
+            po_tree_destroy(*out);
+            *out = nullptr;
+        }
+    }
+    return st;
 }
 
 po_status po_tree_destroy(po_tree* t) {
@@ -491,6 +540,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_child_b) cudaFree(t->d_child_b);
     if (t->d_brick) cudaFree(t->d_brick);
     if (t->d_plan) cudaFree(t->d_plan);
+    if (t->d_sg) cudaFree(t->d_sg);
     t->d_child = nullptr;
     delete t;
     return PO_OK;
@@ -707,6 +757,7 @@ po_status po_backward_plan(po_tree* t, const uint32_t* leaf_span, int64_t n, int
     std::lock_guard<std::mutex> lk(t->plan_mu);
     if (t->plan_cap < need) {
         if (t->d_plan) cudaFree(t->d_plan);
+    if (t->d_sg) cudaFree(t->d_sg);
         t->d_plan = nullptr;
         t->plan_cap = 0;
         e = cudaMalloc(&t->d_plan, need);

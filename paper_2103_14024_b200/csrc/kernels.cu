@@ -28,7 +28,7 @@ struct FwdVisitor {
     float T, gamma;
     float C[3];
     __device__ FwdVisitor(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g) {
-        sh_basis<DEG>(d, t.odd_sign, Y);
+        ray_basis<DEG>(t, d, Y);
         C[0] = C[1] = C[2] = 0.f;
     }
     __device__ __forceinline__ void on_node() {}
@@ -60,7 +60,7 @@ struct FwdVisitorPipe {
     float4 row[NV];
     float wpend;   // weight of the pending leaf (0: none)
     __device__ FwdVisitorPipe(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g), wpend(0.f) {
-        sh_basis<DEG>(d, t.odd_sign, Y);
+        ray_basis<DEG>(t, d, Y);
         C[0] = C[1] = C[2] = 0.f;
     }
     __device__ __forceinline__ void on_node() {}
@@ -110,7 +110,7 @@ struct FwdVisitorSm {
     float* stage;   // this thread's slot
     __device__ FwdVisitorSm(const DevTree& t, const float d[3], float g, float* st)
         : tr(t), T(1.f), gamma(g), stage(st) {
-        sh_basis<DEG>(d, t.odd_sign, Y);
+        ray_basis<DEG>(t, d, Y);
         C[0] = C[1] = C[2] = 0.f;
     }
     __device__ __forceinline__ void on_node() {}
@@ -184,7 +184,7 @@ struct TotalVisitor {
     int32_t nseg, max_seg;      // max_seg < 0: no segment bookkeeping
     __device__ TotalVisitor(const DevTree& t, const float d[3], float g)
         : tr(t), T(1.f), gamma(g), lo(0xFFFFFFFFu), hi(0u), seg(nullptr), seg_stride(0), nseg(0), max_seg(-1) {
-        sh_basis<DEG>(d, t.odd_sign, Y);
+        ray_basis<DEG>(t, d, Y);
         C[0] = C[1] = C[2] = 0.0;
     }
     __device__ __forceinline__ void on_node() {}
@@ -230,7 +230,7 @@ struct GradVisitor {
     float* __restrict__ grad_sh;
     __device__ GradVisitor(const DevTree& t, const float d[3], float gm, float* gs, float* gk)
         : tr(t), T(1.f), gamma(gm), grad_sigma(gs), grad_sh(gk) {
-        sh_basis<DEG>(d, t.odd_sign, Y);
+        ray_basis<DEG>(t, d, Y);
         P[0] = P[1] = P[2] = 0.0;
     }
     __device__ __forceinline__ void on_node() {}
@@ -684,7 +684,7 @@ __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __res
     for (int k = 0; k < 3; ++k) dir[k] = __ldg(rays + i * 6 + 3 + k);
     if (!unit_direction(dir, d)) return;
     float Y[B];
-    sh_basis<DEG>(d, tr.odd_sign, Y);
+    ray_basis<DEG>(tr, d, Y);
     double Ctot[3], carry[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) Ctot[ch] = aux[i * 4 + ch];

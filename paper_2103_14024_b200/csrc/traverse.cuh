@@ -58,6 +58,9 @@ struct DevTree {
     const uint32_t* __restrict__ child_b;
     const uint32_t* __restrict__ brick;   // [n_bricks][64], index (x&3)*16 + (y&3)*4 + (z&3)
     uint32_t brick_root;
+    // NEXT f3, spherical Gaussians: B lobes (unit axis xyz, bandwidth) replacing
+    // the SH basis when non-null (po_tree_set_sg_basis)
+    const float4* __restrict__ sg;
 };
 // brick entry with tag 3: a whole level-(D-1) box; bit 29 set = it is one leaf (index in 28:0)
 constexpr uint32_t kBrickLeafBit = 1u << 29;
@@ -366,6 +369,22 @@ __device__ __forceinline__ void sh_basis(const float d[3], float odd, float* Y) 
                 Y[24] = 0.62583573544917614f * (xx * (xx - 3.f * yy) - yy * (3.f * xx - yy));
             }
         }
+    }
+}
+
+// The per-ray basis of the tree: SH (App. B.1) or, when the tree carries lobes, spherical
+// Gaussians G_b(d) = exp(lambda_b (d . p_b - 1)), B = (DEG + 1)^2 of them.
+template <int DEG>
+__device__ __forceinline__ void ray_basis(const DevTree& tr, const float d[3], float* Y) {
+    if (tr.sg != nullptr) {
+        constexpr int B = ShDim<DEG>::B;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const float4 p = __ldg(tr.sg + b);
+            Y[b] = expf(p.w * (fmaf(d[0], p.x, fmaf(d[1], p.y, d[2] * p.z)) - 1.f));
+        }
+    } else {
+        sh_basis<DEG>(d, tr.odd_sign, Y);
     }
 }
 

@@ -99,3 +99,45 @@ def test_c1_depth_and_filter_sampled(env, c1_tree):
     want = om.leaf_max_alpha(ot, rays.astype(np.float64), gamma=0.01)
     assert np.abs(got - want).max() <= 2e-3
     assert ((got > 0) == (want > 0)).mean() > 0.999
+
+
+def _sg_lobes(B, seed):
+    g = np.random.default_rng(seed)
+    p = g.normal(size=(B, 3))
+    p /= np.linalg.norm(p, axis=1, keepdims=True)
+    return p.astype(np.float32), g.uniform(0.5, 20.0, size=B).astype(np.float32)
+
+
+@pytest.mark.parametrize("deg,gamma", [(4, 0.01), (4, 0.0), (2, 0.01)])
+def test_sg_basis_render_and_backward(env, deg, gamma):
+    """NEXT f3 SG-25: render and backward with spherical-Gaussian lobes against the
+    oracle on the same (fp32) lobes; SH restored afterwards."""
+    po, om, torch = env
+    t = gen.scene_random(73 + deg, depth=5, sh_degree=deg, sigma_scale=3.0)
+    B = (deg + 1) ** 2
+    axes, lam = _sg_lobes(B, 9)
+    tree = po.tree_from_gen(t)
+    tree.set_sg_basis(axes, lam)
+    # the oracle normalises in double what the library normalises in fp32 -> hand it the same axes
+    ax32 = (axes.astype(np.float64) / np.linalg.norm(axes.astype(np.float64), axis=1, keepdims=True))
+    ot = om.OracleTree(t, sg=(ax32, lam.astype(np.float64)))
+    rays = gen.random_rays(74, 3000, inside_frac=0.1).astype(np.float64)
+    rays = rays[_tie_free(om, ot, rays, gamma)]
+    r = torch.from_numpy(rays.astype(np.float32)).cuda()
+    out = po.po_render_rays(tree, r, gamma=gamma).cpu().numpy()
+    ref = om.render(ot, rays.astype(np.float32).astype(np.float64), gamma=gamma)
+    assert np.abs(out - ref["rgb"]).max() <= TOL
+    g = np.random.default_rng(10).normal(size=(rays.shape[0], 3)).astype(np.float32)
+    gs = torch.zeros(tree.n_leaves, device="cuda")
+    gk = torch.zeros((tree.n_leaves, B, 3), device="cuda")
+    po.po_render_backward(tree, r, torch.from_numpy(g).cuda(), gs, gk, gamma=gamma)
+    rs, rk = om.backward(ot, rays.astype(np.float32).astype(np.float64), g.astype(np.float64), gamma=gamma)
+    for a, b, tag in ((gs.cpu().numpy(), rs, "sigma"), (gk.cpu().numpy(), rk, "sg coefficients")):
+        a, b = a.ravel().astype(np.float64), b.ravel()
+        assert np.linalg.norm(a - b) <= 1e-3 * np.linalg.norm(b), tag
+    # back to SH: identical to a fresh SH tree
+    tree.set_sg_basis(None)
+    sh_out = po.po_render_rays(tree, r, gamma=gamma)
+    assert torch.equal(sh_out, po.po_render_rays(po.tree_from_gen(t), r, gamma=gamma))
+    with pytest.raises(po.PoError):
+        tree.set_sg_basis(np.zeros((B, 3), np.float32), lam)
