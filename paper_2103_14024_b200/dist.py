@@ -97,3 +97,23 @@ def overlapped_chunks(flat, leaf_end, n_leaves: int, basis_dim: int, sh_offset: 
         for b, e in pr:
             if e > b:
                 apply_final(b, e)
+
+
+def agree_bounds(bounds, n_leaves: int, group=None, world_size: int = 1):
+    """Leaf bounds every rank will use: the mean of the ranks' calibrated bounds, floored.  The
+    allreduce ranges of overlapped_chunks must be identical on all ranks (a collective of
+    mismatched sizes fails), while each rank calibrates on its own rays.  A mean of
+    non-decreasing sequences is non-decreasing and the last bound stays n_leaves."""
+    b = [int(x) for x in bounds]
+    if world_size <= 1:
+        return b
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(b, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    out = [int(v) for v in torch.floor(t / world_size).tolist()]
+    out[-1] = int(n_leaves)
+    for j in range(1, len(out)):
+        out[j] = max(out[j], out[j - 1])
+    return out

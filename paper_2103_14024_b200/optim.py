@@ -24,7 +24,7 @@ import torch
 
 from . import (Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk, po_render_rays,
                po_tree_sgd_step_range)
-from .dist import allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets
+from .dist import agree_bounds, allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets
 
 
 class OctreeOptimizer:
@@ -95,7 +95,7 @@ class OctreeOptimizer:
                 # first chunked step: one host sync to read this batch's ray quantiles; later
                 # steps reuse them as leaf bounds (equal-work chunks; batches of one scene
                 # have similar first-leaf distributions, and any bounds are correct)
-                self.leaf_bounds[K] = quant.cpu().tolist()
+                self.leaf_bounds[K] = agree_bounds(quant.cpu().tolist(), nl, self.group, self.world_size)
             # chunks alternate between two side streams so one chunk's tail (its slowest rays)
             # overlaps the next chunk; the current stream joins chunk j before the allreduce of
             # the range chunk j finalises is enqueued on it (gradient atomics commute, so

@@ -9,8 +9,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2103_14024_b200.dist import (allreduce_buckets, flat_layout, flat_to_param_range, leaf_range_slices,
-                                        overlapped_chunks, plan_buckets)
+from paper_2103_14024_b200.dist import (agree_bounds, allreduce_buckets, flat_layout, flat_to_param_range,
+                                        leaf_range_slices, overlapped_chunks, plan_buckets)
 
 
 def test_plan_covers_exactly_once():
@@ -175,3 +175,30 @@ def test_overlapped_chunks_world2_equals_full_sum():
         np.testing.assert_allclose(params, want, rtol=0, atol=1e-9)
         cov = sorted(x for b, e in seen for x in range(b, e))
         assert cov == list(range(n * (1 + ne)))
+
+
+def _bounds_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 1000
+    local = [[100, 400, 401, 1000], [300, 350, 900, 1000]][rank]   # each rank's own quantiles
+    q.put((rank, agree_bounds(local, n, None, world)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_agree_bounds_world2_identical_and_monotone():
+    """Ranks calibrate chunk bounds on their own rays; the allreduce ranges must match, so the
+    bounds are agreed (mean, floored, monotone, last = n_leaves) before use."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_bounds_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] == [200, 375, 650, 1000]
