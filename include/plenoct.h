@@ -122,7 +122,10 @@ po_status po_render(const po_tree* tree, const po_camera* cams, int32_t n_cams, 
                     const po_render_opts* opts, float* out_rgb, po_stream stream);
 
 /* Same as po_render with HOST cameras and a HOST output image: copies the cameras in,
- * renders, copies the image out and synchronises the stream (end-to-end entry point). */
+ * renders, copies the image out and synchronises the stream (end-to-end entry point).  If
+ * out_rgb_host is pinned (cudaHostAlloc / torch pin_memory: device-mapped under unified
+ * addressing) the kernel writes the pixels straight into it over PCIe while rendering
+ * (PO_HOST_DIRECT=0 forces the staged copy); pageable memory is staged and copied. */
 po_status po_render_host(const po_tree* tree, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
                          const po_render_opts* opts, float* out_rgb_host, po_stream stream);
 

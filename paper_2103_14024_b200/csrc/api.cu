@@ -651,6 +651,28 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
     cudaError_t e = cudaMemcpyAsync(t->d_cams, cams_host, sizeof(po_camera) * (size_t)n_cams, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_status(e, "H2D cams");
     const size_t out_bytes = (size_t)n_cams * W * H * 3 * sizeof(float);
+    // A pinned (page-locked, device-mapped) output buffer is written by the kernel itself over
+    // PCIe while it renders, so the image transfer overlaps the render instead of following
+    // it; pageable buffers go through the device scratch image and one D2H copy.
+    static const bool direct_ok = [] {
+        const char* ev = getenv("PO_HOST_DIRECT");
+        return !(ev && std::strcmp(ev, "0") == 0);
+    }();
+    float* direct = nullptr;
+    if (direct_ok) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr)
+            direct = static_cast<float*>(pa.devicePointer);
+        else
+            (void)cudaGetLastError();   // pageable memory: not an error
+    }
+    if (direct) {
+        po_status st = render_scheduled(t, t->d_cams, n_cams, W, H, o, direct, s, "po_render_host");
+        e = cudaStreamSynchronize(s);
+        if (st == PO_OK && e != cudaSuccess) st = cuda_status(e, "sync");
+        return st;
+    }
     if (t->img_cap < out_bytes) {   // grows once; later calls reuse it (no per-call allocation)
         e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return cuda_status(e, "sync");

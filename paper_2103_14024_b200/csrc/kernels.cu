@@ -394,6 +394,38 @@ cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, 
     return cudaGetLastError();
 }
 
+// Store an 8x4 warp tile's RGB (lane = pixel: x = lane & 7, y = lane >> 3).  When the tile is
+// whole and rows are 16-B aligned (W % 4 == 0), the 4 rows x 96 contiguous bytes go out as
+// 24 float4 stores assembled with shuffles (whole 16-B words also when `out` is pinned host
+// memory written over PCIe by po_render_host); otherwise (edge tiles, odd W, a buffer not
+// 16-B aligned) 3 scalar stores per pixel.
+__device__ __forceinline__ void store_tile_rgb(float* __restrict__ out, size_t row0, int W, int H, int px0, int py0,
+                                               const float C[3]) {
+    const int lane = threadIdx.x & 31;
+    if (px0 + 8 <= W && py0 + 4 <= H && (W & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+        const int r = lane / 6, q = lane - 6 * (lane / 6);   // lanes 0..23: row r, float4 q of 6
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int f = 4 * q + k, src = 8 * r + f / 3, ch = f % 3;
+            const float c0 = __shfl_sync(0xFFFFFFFFu, C[0], src & 31);
+            const float c1 = __shfl_sync(0xFFFFFFFFu, C[1], src & 31);
+            const float c2 = __shfl_sync(0xFFFFFFFFu, C[2], src & 31);
+            v[k] = ch == 0 ? c0 : (ch == 1 ? c1 : c2);
+        }
+        if (lane < 24)
+            reinterpret_cast<float4*>(out + ((row0 + py0 + r) * W + px0) * 3)[q] = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+        const int px = px0 + (lane & 7), py = py0 + (lane >> 3);
+        if (px < W && py < H) {
+            float* p = out + ((row0 + py) * W + px) * 3;
+            p[0] = C[0];
+            p[1] = C[1];
+            p[2] = C[2];
+        }
+    }
+}
+
 // CTA = 16x16 pixels = 8 warps, each warp an 8x4 pixel tile (warp-coherent ray packets).
 __device__ __forceinline__ bool tile_pixel(int W, int H, int& px, int& py) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -464,11 +496,11 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
         const int px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
         const int py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
+        float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
         if (px < W && py < H) {
             float o[3], d[3];
             camera_ray(cams, (int)view, px, py, o, d);
             RayState r;
-            float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
             if (ray_setup(tr, o, d, r)) {
                 if constexpr ((OPT & kOptSmemRow) != 0) {
                     extern __shared__ __align__(16) float po_dyn_smem[];
@@ -505,11 +537,8 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
             }
-            float* p = out + (((size_t)view * H + py) * W + px) * 3;
-            p[0] = C[0];
-            p[1] = C[1];
-            p[2] = C[2];
         }
+        store_tile_rgb(out, (size_t)view * H, W, H, bx * 16 + (int)(sub & 1u) * 8, by * 16 + (int)(sub >> 1) * 4, C);
         if (timeline != nullptr) {   // measurement mode (po_render_timeline): one record per warp tile
             __syncwarp();
             if (lane == 0) {

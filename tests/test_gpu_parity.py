@@ -159,8 +159,11 @@ def test_multi_view_batch_and_host_path(env, c0_tree):
     tree = po.tree_from_gen(c0_tree)
     cams = np.concatenate([gen.orbit_camera(3.0, 23.4 + 40 * i, 17.9, 64, 64, 70.0) for i in range(5)])
     dev = po.po_render(tree, po.cams_tensor(cams), 64, 64).cpu().numpy()
-    host = po.po_render_host(tree, cams, 64, 64)
+    host = po.po_render_host(tree, cams, 64, 64)            # pageable: staged + D2H copy
     assert np.array_equal(dev, host)
+    pinned = torch.empty((5, 64, 64, 3), dtype=torch.float32, pin_memory=True).numpy()
+    po.po_render_host(tree, cams, 64, 64, out_host=pinned)   # pinned: the kernel writes it directly
+    assert np.array_equal(dev, pinned)
     ot = om.OracleTree(c0_tree)
     for i in range(5):
         rays = om.camera_rays(cams[i:i + 1], 64, 64)
