@@ -349,6 +349,14 @@ def run_c4(args):
             mx = gen.trees._part1by2(x) | (gen.trees._part1by2(y) << np.uint64(1))
             pick = pick[np.argsort((view.astype(np.uint64) << np.uint64(44)) | mx, kind="stable")]
         rays = torch.from_numpy(gen.camera_rays_f32(cams, W, H, pick // (W * H), pick % (W * H))).to(dev)
+        if args.ray_order == "tileleaf" and args.ray_sampling == "tile":
+            # keep each 8x4 tile's 32 rays together (warp coherence) and order the TILES by
+            # the lowest first-entered leaf among their rays (inter-warp locality)
+            ids, _, _ = po.po_trace(gt, rays, max_leaves=1, gamma=0.0, with_nodes=False)
+            key = ids[:, 0].to(torch.int64)
+            key = torch.where(key < 0, torch.full_like(key, 1 << 40), key).view(-1, 32).min(dim=1).values
+            order = torch.argsort(key, stable=True)
+            rays = rays.view(-1, 32, 6)[order].reshape(-1, 6).contiguous()
         if args.ray_order == "leaf":
             # batch preparation: order rays by the first leaf they enter.  The tree structure is
             # fixed during optimisation, so this key is a per-pixel constant; leaves are
@@ -399,6 +407,28 @@ def run_c4(args):
         t_max = float(tt.item())
     K = args.steps
     rays_per_s = ws * K * n_rays / (t_max / 1e3)
+
+    # e2e: the same steps through the public API from pinned HOST batches: every step copies its
+    # rays + targets host -> device inside the timed region and reads the loss back (D2H)
+    e2e_steps = min(K, 10)
+    host = [(b[0].cpu().pin_memory(), b[1].cpu().pin_memory()) for b in batches[args.warmup:args.warmup + e2e_steps]]
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for hr, ht in host:
+        loss = opt.step(hr.to(dev, non_blocking=True), ht.to(dev, non_blocking=True))
+        float(loss.item())
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if ws > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = ws * e2e_steps * n_rays / (e2e_ms / 1e3)
     if rank == 0:
         peak, peak_src = _peaks()
         alg = (visits * (4 + 192 + 196) + nodes * 32) / K + n_rays * (24 + 12 + 32)
@@ -422,6 +452,9 @@ def run_c4(args):
                          "achieved_step": round(alg / (t_max / K / 1e3) / 1e9, 1),
                          "alg_bytes_def": "visits*(4 sigma + 192 SH row + 196 gradient RMW) + nodes*32 + rays*68"},
             "gpu_launches": int(launches), "clocks": clk,
+            "e2e": {"value": round(e2e_value, 1), "unit": "rays/s", "h2d_bytes_per_step": n_rays * (24 + 12),
+                    "d2h_bytes_per_step": 8, "entry": "OctreeOptimizer.step on pinned host batches (H2D rays + "
+                                                      "targets, loss read back every step)"},
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -507,7 +540,7 @@ def main():
                     help="c4: pass-2 chunks overlapped with the allreduce (default 4 if N>1, else 1)")
     ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
-    ap.add_argument("--ray-order", choices=["sampled", "leaf"], default="leaf",
+    ap.add_argument("--ray-order", choices=["sampled", "leaf", "tileleaf"], default="leaf",
                     help="c4: keep the sampled order or sort the batch by first-entered leaf")
     ap.add_argument("--ray-sampling", choices=["tile", "pixel"], default="tile",
                     help="c4: sample 8x4 pixel tiles (coherent warps) or single pixels")
