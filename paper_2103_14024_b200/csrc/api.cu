@@ -31,14 +31,6 @@ struct po_tree {
     int cam_cap = 0;
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
-    uint32_t root_entry = 0;       // device entry word of the root (traverse.cuh encoding)
-    uint32_t* d_child_b = nullptr; // child table whose level-(D-2) targets are brick indices
-    uint32_t* d_brick = nullptr;   // [n_bricks][64] flattened bottom two levels
-    uint32_t brick_root = 0;
-    bool node_masks = false;       // internal entries carry the child's occupancy mask
-    // empty-space skipping grid (DevTree::macro): level M = min(5, D - 1)
-    uint8_t* d_macro = nullptr;
-    int macro_level = 0;
     // centre-out order of the 16x16 pixel blocks of a W x H view (built once per size)
     unsigned* d_order = nullptr;
     int order_w = 0, order_h = 0;
@@ -132,9 +124,6 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
 po::DevTree dev_tree(const po_tree* t) {
     po::DevTree d;
     d.child = t->d_child;
-    d.root_entry = t->root_entry;
-    d.node_masks = t->node_masks ? 1 : 0;
-    d.node_idx_mask = t->node_masks ? po::kMaskedIdx : po::kIdxMask;
     d.sigma = t->d_sigma;
     d.sh = t->d_sh;
     d.sh_row = t->sh_row;
@@ -142,71 +131,8 @@ po::DevTree dev_tree(const po_tree* t) {
     for (int k = 0; k < 3; ++k) d.bmin[k] = t->desc.bbox_min[k];
     d.scale = (float)std::ldexp(1.0, t->desc.max_depth) / t->desc.bbox_edge;
     d.odd_sign = t->desc.sh_sign == PO_SH_NO_CS ? -1.f : 1.f;
-    d.child_b = t->d_child_b;
-    d.brick = t->d_brick;
-    d.brick_root = t->brick_root;
-    d.macro = t->d_macro;
-    d.macro_shift = t->desc.max_depth - t->macro_level;
-    d.macro_n = 1 << t->macro_level;
     d.sg = t->d_sg;
     return d;
-}
-
-// Level-M occupancy of the leaves and its Chebyshev distance transform (multi-source BFS over
-// the 26-neighbourhood), capped at 255.  Host side, once per tree (a0).
-std::vector<uint8_t> build_macro_grid(const uint32_t* child, int D, int M) {
-    const int n = 1 << M;
-    std::vector<uint8_t> occ((size_t)n * n * n, 0);
-    struct Item { uint32_t node; int level; int x, y, z; };
-    std::vector<Item> st{{0u, 0, 0, 0, 0}};
-    while (!st.empty()) {
-        const Item it = st.back();
-        st.pop_back();
-        for (int o = 0; o < 8; ++o) {
-            const uint32_t e = child[(size_t)it.node * 8 + o];
-            const uint32_t tag = e >> 30;
-            if (tag == po::kTagEmpty) continue;
-            const int L = it.level + 1;
-            const int x = it.x * 2 + ((o >> 2) & 1), y = it.y * 2 + ((o >> 1) & 1), z = it.z * 2 + (o & 1);
-            if (tag == po::kTagInternal) {
-                st.push_back({e & po::kIdxMask, L, x, y, z});
-            } else if (L >= M) {
-                const int s = L - M;
-                occ[((size_t)(x >> s) * n + (y >> s)) * n + (z >> s)] = 1;
-            } else {
-                const int s = M - L;
-                for (int a = x << s; a < (x + 1) << s; ++a)
-                    for (int b = y << s; b < (y + 1) << s; ++b)
-                        for (int c = z << s; c < (z + 1) << s; ++c) occ[((size_t)a * n + b) * n + c] = 1;
-            }
-        }
-    }
-    std::vector<uint8_t> dist((size_t)n * n * n, 255);
-    std::vector<int> frontier, next;
-    for (size_t i = 0; i < occ.size(); ++i)
-        if (occ[i]) {
-            dist[i] = 0;
-            frontier.push_back((int)i);
-        }
-    for (int d = 1; d < 255 && !frontier.empty(); ++d) {
-        next.clear();
-        for (int i : frontier) {
-            const int a = i / (n * n), b = (i / n) % n, c = i % n;
-            for (int da = -1; da <= 1; ++da)
-                for (int db = -1; db <= 1; ++db)
-                    for (int dc = -1; dc <= 1; ++dc) {
-                        const int aa = a + da, bb = b + db, cc = c + dc;
-                        if (aa < 0 || bb < 0 || cc < 0 || aa >= n || bb >= n || cc >= n) continue;
-                        const size_t j = ((size_t)aa * n + bb) * n + cc;
-                        if (dist[j] == 255) {
-                            dist[j] = (uint8_t)d;
-                            next.push_back((int)j);
-                        }
-                    }
-        }
-        frontier.swap(next);
-    }
-    return dist;
 }
 
 po_status check_opts(const po_render_opts* o, po::RenderOpts* out) {
@@ -331,85 +257,12 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sigma)"));
     e = cudaMalloc(&t->d_sh, (size_t)std::max<int64_t>(n_leaves, 1) * row * elt);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
-    {
-        t->macro_level = std::min(5, D - 1);
-        const std::vector<uint8_t> grid = build_macro_grid(child, D, t->macro_level);
-        e = cudaMalloc(&t->d_macro, grid.size());
-        if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(macro)"));
-        e = cudaMemcpy(t->d_macro, grid.data(), grid.size(), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return cleanup(cuda_status(e, "upload macro"));
-    }
     e = cudaMalloc(&t->d_work, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
     e = cudaMemset(t->d_work, 0, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "memset(work)"));
-    {
-        // device child table: internal entries carry the child node's occupancy mask so the
-        // descent knows an empty octant without loading it (traverse.cuh, kMaskShift)
-        static const bool masks_off = [] {
-            const char* ev = getenv("PO_NODE_MASKS");
-            return ev && std::strcmp(ev, "0") == 0;
-        }();
-        t->node_masks = !masks_off && n_nodes <= ((int64_t)1 << po::kMaskShift);
-        std::vector<uint32_t> occ((size_t)n_nodes, 0);
-        for (int64_t i = 0; i < n_nodes; ++i)
-            for (int o = 0; o < 8; ++o) occ[i] |= (uint32_t)((child[i * 8 + o] >> 30) != po::kTagEmpty) << o;
-        std::vector<uint32_t> dev((size_t)n_nodes * 8);
-        for (size_t i = 0; i < dev.size(); ++i) {
-            const uint32_t en = child[i];
-            dev[i] = (t->node_masks && (en >> 30) == po::kTagInternal)
-                         ? (po::kTagInternal << 30) | (occ[en & po::kIdxMask] << po::kMaskShift) | (en & po::kIdxMask)
-                         : en;
-        }
-        t->root_entry = (po::kTagInternal << 30) | (t->node_masks ? occ[0] << po::kMaskShift : 0u);
-        e = cudaMemcpy(t->d_child, dev.data(), dev.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-        // bricks (opt-in experiment, PO_BRICKS=1; measured slower): each
-        // level-(D-2) node gets a 4x4x4 brick of its leaf-level cells
-        static const bool bricks_on = [] {
-            const char* ev = getenv("PO_BRICKS");
-            return ev && std::strcmp(ev, "1") == 0;
-        }();
-        const int Lb = D - 2;
-        if (e == cudaSuccess && bricks_on && Lb >= 0 && n_leaves <= (int64_t)po::kBrickLeafBit) {
-            const uint32_t idx_mask = t->node_masks ? po::kMaskedIdx : po::kIdxMask;
-            std::vector<uint32_t> bid((size_t)n_nodes, 0xFFFFFFFFu);
-            uint32_t nb = 0;
-            for (int64_t i = 0; i < n_nodes; ++i)
-                if (node_level[(size_t)i] == Lb) bid[(size_t)i] = nb++;
-            std::vector<uint32_t> brick((size_t)nb * 64, 0);
-            for (int64_t i = 0; i < n_nodes; ++i) {
-                if (bid[(size_t)i] == 0xFFFFFFFFu) continue;
-                uint32_t* b = brick.data() + (size_t)bid[(size_t)i] * 64;
-                for (int o1 = 0; o1 < 8; ++o1) {
-                    const uint32_t e1 = child[i * 8 + o1];
-                    const int x1 = (o1 >> 2) & 1, y1 = (o1 >> 1) & 1, z1 = o1 & 1;
-                    for (int o2 = 0; o2 < 8; ++o2) {
-                        const int x = 2 * x1 + ((o2 >> 2) & 1), y = 2 * y1 + ((o2 >> 1) & 1), z = 2 * z1 + (o2 & 1);
-                        uint32_t v;
-                        if ((e1 >> 30) == po::kTagEmpty)
-                            v = 3u << 30;   // empty level-(D-1) box
-                        else if ((e1 >> 30) == po::kTagLeaf)
-                            v = (3u << 30) | po::kBrickLeafBit | (e1 & po::kIdxMask);   // one coarser leaf
-                        else
-                            v = child[(size_t)(e1 & po::kIdxMask) * 8 + o2];   // leaf-level leaf or empty
-                        b[x * 16 + y * 4 + z] = v;
-                    }
-                }
-            }
-            std::vector<uint32_t> devb(dev);
-            for (size_t j = 0; j < devb.size(); ++j) {
-                const uint32_t en = child[j];
-                if ((en >> 30) == po::kTagInternal && bid[en & po::kIdxMask] != 0xFFFFFFFFu)
-                    devb[j] = (devb[j] & ~idx_mask) | bid[en & po::kIdxMask];
-            }
-            t->brick_root = Lb == 0 ? ((po::kTagInternal << 30) | bid[0]) : t->root_entry;
-            if ((e = cudaMalloc(&t->d_child_b, devb.size() * sizeof(uint32_t))) == cudaSuccess &&
-                (e = cudaMalloc(&t->d_brick, std::max<size_t>(brick.size(), 1) * sizeof(uint32_t))) == cudaSuccess &&
-                (e = cudaMemcpy(t->d_child_b, devb.data(), devb.size() * sizeof(uint32_t),
-                                cudaMemcpyHostToDevice)) == cudaSuccess && !brick.empty())
-                e = cudaMemcpy(t->d_brick, brick.data(), brick.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-        }
-    }
+    // the device child table is the caller's (ABI encoding, reading Q1)
+    e = cudaMemcpy(t->d_child, child, (size_t)n_nodes * 8 * sizeof(uint32_t), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "upload child"));
     if (n_leaves > 0) {
         e = cudaMemcpy(t->d_sigma, sigma, (size_t)n_leaves * sizeof(float), cudaMemcpyHostToDevice);
@@ -536,9 +389,6 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_work) cudaFree(t->d_work);
     if (t->d_img) cudaFree(t->d_img);
     if (t->d_order) cudaFree(t->d_order);
-    if (t->d_macro) cudaFree(t->d_macro);
-    if (t->d_child_b) cudaFree(t->d_child_b);
-    if (t->d_brick) cudaFree(t->d_brick);
     if (t->d_plan) cudaFree(t->d_plan);
     if (t->d_sg) cudaFree(t->d_sg);
     t->d_child = nullptr;

@@ -45,121 +45,6 @@ struct FwdVisitor {
     }
 };
 
-// Forward visitor that software-pipelines the leaf rows: early termination needs only
-// sigma~ and delta (T_{i+1} = T_i e^{-sigma delta}), so the 12 row loads of leaf i are issued
-// when the ray reaches it and consumed only at the next leaf (or at the end of the ray); their
-// latency overlaps the box steps in between.  fp32 payload only.
-template <int DEG>
-struct FwdVisitorPipe {
-    static constexpr int NE = 3 * ShDim<DEG>::B;
-    static constexpr int NV = (NE + 3) / 4;
-    const DevTree& tr;
-    float Y[ShDim<DEG>::B];
-    float T, gamma;
-    float C[3];
-    float4 row[NV];
-    float wpend;   // weight of the pending leaf (0: none)
-    __device__ FwdVisitorPipe(const DevTree& t, const float d[3], float g) : tr(t), T(1.f), gamma(g), wpend(0.f) {
-        ray_basis<DEG>(t, d, Y);
-        C[0] = C[1] = C[2] = 0.f;
-    }
-    __device__ __forceinline__ void on_node() {}
-    __device__ __forceinline__ void consume() {
-        float z[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const float vv[4] = {row[j].x, row[j].y, row[j].z, row[j].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int el = 4 * j + q;
-                if (el < NE) z[el % 3] = fmaf(vv[q], Y[el / 3], z[el % 3]);
-            }
-        }
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(wpend, sigmoidf_(z[ch]), C[ch]);
-    }
-    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
-        const float st = __ldg(tr.sigma + idx);
-        if (wpend != 0.f) consume();
-        wpend = 0.f;
-        if (!(st > 0.f)) return true;
-        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(tr.sh) + (size_t)idx * tr.sh_row);
-#pragma unroll
-        for (int j = 0; j < NV; ++j) row[j] = __ldg(src + j);
-        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
-        wpend = a.w;
-        T = a.Tn;
-        return !(T < gamma);
-    }
-    __device__ __forceinline__ void finish() {
-        if (wpend != 0.f) consume();
-        wpend = 0.f;
-    }
-};
-
-// Forward visitor whose leaf rows land in shared memory through cp.async (LDGSTS) instead of
-// 48 registers: the row loads stay fully in flight while the kernel fits 3 CTAs (24 warps)
-// per SM instead of 2.  Each thread owns a 208-B slot (52 words: conflict-free LDS.128).
-constexpr int kStageWords = 52;
-template <int DEG, bool F16>
-struct FwdVisitorSm {
-    const DevTree& tr;
-    float Y[ShDim<DEG>::B];
-    float T, gamma;
-    float C[3];
-    float* stage;   // this thread's slot
-    __device__ FwdVisitorSm(const DevTree& t, const float d[3], float g, float* st)
-        : tr(t), T(1.f), gamma(g), stage(st) {
-        ray_basis<DEG>(t, d, Y);
-        C[0] = C[1] = C[2] = 0.f;
-    }
-    __device__ __forceinline__ void on_node() {}
-    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
-        constexpr int NE = 3 * ShDim<DEG>::B;
-        constexpr int NB = F16 ? (NE * 2 + 15) / 16 : (NE * 4 + 15) / 16;   // 16-B chunks per row
-        const char* src = static_cast<const char*>(tr.sh) + (size_t)idx * tr.sh_row * (F16 ? 2 : 4);
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage);
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * j), "l"(src + 16 * j) : "memory");
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        const float st = __ldg(tr.sigma + idx);
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        if (!(st > 0.f)) return true;
-        float z[3] = {0.f, 0.f, 0.f};
-        if (!F16) {
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                const float4 v = *reinterpret_cast<const float4*>(stage + 4 * j);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int el = 4 * j + q;
-                    if (el < NE) z[el % 3] = fmaf(vv[q], Y[el / 3], z[el % 3]);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                const uint4 v = *reinterpret_cast<const uint4*>(stage + 4 * j);
-                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[q]));
-                    const int el0 = 8 * j + 2 * q, el1 = el0 + 1;
-                    if (el0 < NE) z[el0 % 3] = fmaf(f.x, Y[el0 / 3], z[el0 % 3]);
-                    if (el1 < NE) z[el1 % 3] = fmaf(f.y, Y[el1 / 3], z[el1 % 3]);
-                }
-            }
-        }
-        const Absorb a = absorb(T, st, __fsub_rn(t1, t0));
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(a.w, sigmoidf_(z[ch]), C[ch]);
-        T = a.Tn;
-        return !(T < gamma);
-    }
-};
-
 // Stored pass-1 segments (po_segments): record k of ray i = two float4 at (k n + i) * 2:
 // (leaf index bits, delta, w, T_{i+1}), (c_r, c_g, c_b, 0) -- every value pass 2 needs, so it
 // replays the segments instead of re-traversing the tree.  count[i] = number of sigma~ > 0
@@ -502,13 +387,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             camera_ray(cams, (int)view, px, py, o, d);
             RayState r;
             if (ray_setup(tr, o, d, r)) {
-                if constexpr ((OPT & kOptSmemRow) != 0) {
-                    extern __shared__ __align__(16) float po_dyn_smem[];
-                    FwdVisitorSm<DEG, F16> v(tr, r.d, opt.gamma, po_dyn_smem + threadIdx.x * kStageWords);
-                    traverse<OPT & ~kOptSmemRow>(tr, r, v, stk);
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
-                } else if constexpr ((OPT & kOptProbeNoShade) != 0) {
+                if constexpr ((OPT & kOptProbeNoShade) != 0) {
                     // measurement probe only (PO_RENDER_OPT=64, wrong colours): the traversal and
                     // transmittance without any SH row, to size a traversal/shading split
                     struct Probe {
@@ -522,17 +401,11 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                             return !(T < gamma);
                         }
                     } v{tr, 1.f, opt.gamma};
-                    traverse<0>(tr, r, v, stk);
+                    traverse<kOptLean>(tr, r, v, stk);
                     C[0] = C[1] = C[2] = v.T;
-                } else if constexpr ((OPT & kOptPipeRow) != 0 && !F16) {
-                    FwdVisitorPipe<DEG> v(tr, r.d, opt.gamma);
-                    traverse<OPT & ~kOptPipeRow>(tr, r, v, stk);
-                    v.finish();
-#pragma unroll
-                    for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 } else {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                    traverse<OPT & (kOptLeafStep | kOptMacroSkip | kOptNodeMask | kOptLean | kOptBrick)>(tr, r, v, stk);
+                    traverse<OPT & kOptLean>(tr, r, v, stk);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -1108,9 +981,9 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     if (tiles >= (int64_t)0xFFFFFFF0u) return cudaErrorInvalidValue;
     // CTAs per SM the register budget is tuned for.  Default 2 (<= 128 registers): all 12
     // LDG.128 of a leaf row stay in flight, which beat 3-4 CTAs/SM on B200 (r01: 4127 vs 3819
-    // vs 3160 FPS on c1).  For the SH-3 fp32 path PO_RENDER_MINB=1..4 and PO_RENDER_OPT
-    // (traversal variant bits, traverse.cuh; 0 = the plain step, 256/384 need PO_BRICKS=1)
-    // select other instances for A/B experiments.
+    // vs 3160 FPS on c1).  For the SH-3 fp32 path PO_RENDER_MINB=1,3,4 and PO_RENDER_OPT
+    // (0 = the plain neighbour step, 64 = traversal-only probe; traverse.cuh) select other
+    // instances for A/B experiments.
     static const int minb = [] {
         const char* e = getenv("PO_RENDER_MINB");
         const int v = e ? atoi(e) : 2;
@@ -1119,45 +992,24 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
-        return (v == 0 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128 || v == 256 ||
-                v == 384) ? v
-                                                                                                      : kRenderOptDefault;
+        return (v == kOptPlain || v == kOptProbeNoShade || v == kOptLean) ? v : kRenderOptDefault;
     }();
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
                          unsigned long long*);
     KFn fn = nullptr;
-    int o = kRenderOptDefault;
     if (deg == 3 && !f16 && (minb != 2 || vopt != kRenderOptDefault)) {
-        // A/B instances: each variant at 2 CTAs/SM, the default variant at 1/3/4 CTAs/SM
-        static const KFn by_minb[4] = {k_render<3, false, 1, kRenderOptDefault>, nullptr,
+        static const KFn by_minb[4] = {k_render<3, false, 1, kRenderOptDefault>, k_render<3, false, 2, kRenderOptDefault>,
                                        k_render<3, false, 3, kRenderOptDefault>,
                                        k_render<3, false, 4, kRenderOptDefault>};
-        if (minb == 2) {
-            o = vopt;
-            switch (vopt) {
-                case 2: fn = k_render<3, false, 2, 2>; break;
-                case 4: fn = k_render<3, false, 2, 4>; break;
-                case 8: fn = k_render<3, false, 2, 8>; break;
-                case 16: fn = k_render<3, false, 2, 16>; break;
-                case 32: fn = k_render<3, false, 2, 32>; break;
-                case 64: fn = k_render<3, false, 2, 64>; break;
-                case 128: fn = k_render<3, false, 2, 128>; break;
-                case 256: fn = tr.brick ? k_render<3, false, 2, 256> : k_render<3, false, 2, 0>; break;
-                case 384: fn = tr.brick ? k_render<3, false, 2, 384> : k_render<3, false, 2, 128>; break;
-                default: fn = k_render<3, false, 2, 0>; break;
-            }
-        } else if (vopt == kOptProbeNoShade) {
-            static const KFn probe[4] = {k_render<3, false, 1, kOptProbeNoShade>, nullptr,
-                                         k_render<3, false, 3, kOptProbeNoShade>,
-                                         k_render<3, false, 4, kOptProbeNoShade>};
-            fn = probe[minb - 1];
-        } else {
-            fn = by_minb[minb - 1];
-        }
+        static const KFn probe[4] = {k_render<3, false, 1, kOptProbeNoShade>, k_render<3, false, 2, kOptProbeNoShade>,
+                                     k_render<3, false, 3, kOptProbeNoShade>, k_render<3, false, 4, kOptProbeNoShade>};
+        if (vopt == kOptProbeNoShade) fn = probe[minb - 1];
+        else if (vopt == kOptPlain && minb == 2) fn = k_render<3, false, 2, kOptPlain>;
+        else fn = by_minb[minb - 1];
     } else {
         PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kRenderOptDefault>);
     }
-    const size_t dyn = (o & kOptSmemRow) ? sizeof(float) * kStageWords * 256 : 0;
+    const size_t dyn = 0;
     static std::mutex mu;
     static std::map<KFn, int> grids;   // persistent grid size per kernel instance
     int grid;

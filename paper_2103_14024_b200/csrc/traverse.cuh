@@ -27,18 +27,10 @@ namespace po {
 constexpr uint32_t kTagEmpty = 0u, kTagInternal = 1u, kTagLeaf = 2u;
 constexpr uint32_t kIdxMask = (1u << 30) - 1u;
 constexpr int kMaxDepth = 15;
-// Device child-table encoding (a0, po_tree_create).  Leaf entries: 2<<30 | leaf index (as in
-// the ABI).  Internal entries, when the tree has <= 2^22 nodes: 1<<30 | mask<<22 | node index,
-// mask = occupancy of that child node's 8 slots; otherwise the ABI encoding is kept and every
-// slot is treated as possibly occupied.
-constexpr int kMaskShift = 22;
-constexpr uint32_t kMaskedIdx = (1u << kMaskShift) - 1u;
+// The device child table keeps the ABI encoding (reading Q1): tag << 30 | index.
 
 struct DevTree {
-    const uint32_t* __restrict__ child;   // [n_nodes][8], device encoding (above)
-    uint32_t root_entry;                  // entry word of the root (index 0, its mask)
-    uint32_t node_idx_mask;               // kMaskedIdx or kIdxMask
-    int32_t node_masks;                   // 1 if internal entries carry child masks
+    const uint32_t* __restrict__ child;   // [n_nodes][8], tag << 30 | index (reading Q1)
     const float* __restrict__ sigma;      // [n_leaves]   sigma~
     const void* __restrict__ sh;          // [n_leaves][row] fp32 or fp16, rows 16-B aligned
     int32_t sh_row;                       // row stride in elements
@@ -46,24 +38,10 @@ struct DevTree {
     float bmin[3];
     float scale;                          // 2^D / edge
     float odd_sign;                       // +1 (Condon-Shortley reading) or -1
-    // empty-space skipping: Chebyshev distance (in level-M cells, capped at 255) from each
-    // level-M cell to the nearest level-M cell that contains a leaf; [n][n][n], n = 2^M
-    const uint8_t* __restrict__ macro;
-    int32_t macro_shift;                  // D - M
-    int32_t macro_n;                      // 2^M
-    // bricks (kOptBrick): the two bottom levels flattened.  Every level-(D-2) node owns a
-    // 4x4x4 brick of leaf-level entries (leaf, empty cell, or kBrickBox: a level-(D-1) box that
-    // is empty or one coarser leaf); child_b equals child except that entries pointing to a
-    // level-(D-2) node hold its brick index.  brick_root: the root entry word in that table.
-    const uint32_t* __restrict__ child_b;
-    const uint32_t* __restrict__ brick;   // [n_bricks][64], index (x&3)*16 + (y&3)*4 + (z&3)
-    uint32_t brick_root;
     // NEXT f3, spherical Gaussians: B lobes (unit axis xyz, bandwidth) replacing
     // the SH basis when non-null (po_tree_set_sg_basis)
     const float4* __restrict__ sg;
 };
-// brick entry with tag 3: a whole level-(D-1) box; bit 29 set = it is one leaf (index in 28:0)
-constexpr uint32_t kBrickLeafBit = 1u << 29;
 
 struct RayState {
     float o[3];     // origin in grid units
@@ -134,21 +112,17 @@ struct SmemStack {
 // a3: ordered descent.  Calls vis.on_node() for every internal node entered (root
 // included) and vis.on_leaf(idx, t_in, t_out) for every positive-length leaf segment in
 // ray order; traversal stops when on_leaf returns false (early stop) or the ray exits.
-// Traversal variants (compile time, selected by measurement; see kernels.cu launch_render):
-//   kOptLeafStep     fast neighbour step when the box is a single leaf-level cell
-//   (1 was a register copy of the leaf-parent's 8 entries: measured slower, removed)
-constexpr int kOptLeafStep = 2;
-constexpr int kOptSmemRow = 4;   // (render visitor) leaf rows staged in shared memory by cp.async
-// kOptMacroSkip: when the ray enters a level-M cell whose distance d to the nearest occupied
-// level-M cell is >= 1, jump in one step to the exit of the (2d-1)^3 block of level-M cells
-// around it (all empty by definition of d) instead of stepping through the empty octree
-// boxes one by one.  Leaves are never skipped, so the visited sequence is unchanged.
-constexpr int kOptMacroSkip = 8;
-constexpr int kOptPipeRow = 16;   // (render visitor) leaf rows consumed one leaf later (fp32)
-constexpr int kOptNodeMask = 32;  // skip the load of an empty octant using the entry's child mask
-constexpr int kOptProbeNoShade = 64;   // measurement probe: traversal + T only (not a renderer)
-constexpr int kOptLean = 128;          // leaner neighbour step (see traverse)
-constexpr int kOptBrick = 256;         // bottom two levels through 4x4x4 bricks (DevTree::brick)
+// Neighbour-step variants (compile time; DESIGN.md §6.1 logs the others that were measured
+// slower and removed: leaf-step fast path, shared-memory / pipelined rows, macro-grid skip,
+// child occupancy masks, 4x4x4 bricks, shared-memory upper levels):
+//   kOptPlain = 0      the exit axis steps exactly, the other two are point-located with the
+//                      "moving down onto an integral plane" correction and clamped into the box
+//   kOptLean           every axis whose face is crossed at t_exit steps (an exact edge or corner
+//                      crossing moves diagonally), the others take one F2I.FLOOR and the clamp
+//   kOptProbeNoShade   (render only) measurement probe: traversal + T, no SH rows
+constexpr int kOptPlain = 0;
+constexpr int kOptProbeNoShade = 64;
+constexpr int kOptLean = 128;
 // Default traversal of every kernel (render, render_rays, backward, trace, stats), so all
 // entry points visit the same leaf segments with the same t values (po_render ==
 // po_render_rays bitwise).  Lean measured +2-3% on c1 over the plain step.
@@ -170,85 +144,19 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     int c[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) c[k] = min(max(cell_of(r.o[k], r.dg[k], t), 0), G - 1);
-    constexpr bool kBricks = (OPT & kOptBrick) != 0;
-    const uint32_t* __restrict__ child = kBricks ? tr.child_b : tr.child;
-    const int Lb = D - 2;   // brick-owner level (kBricks)
-    stk[0] = kBricks ? tr.brick_root : tr.root_entry;
+    stk[0] = kTagInternal << 30;   // the root, node 0
     int L = 0;
     vis.on_node();
-    bool check_macro = (OPT & kOptMacroSkip) != 0 && tr.macro != nullptr;
     while (true) {
-        if constexpr ((OPT & kOptMacroSkip) != 0) {
-            if (check_macro) {
-                const int ms = tr.macro_shift, mn = tr.macro_n;
-                const int m0 = c[0] >> ms, m1 = c[1] >> ms, m2 = c[2] >> ms;
-                const int dist = __ldg(tr.macro + ((m0 * mn + m1) * mn + m2));
-                if (dist > 0) {
-                    const int rr = dist - 1;
-                    const int mm[3] = {m0, m1, m2};
-                    int lo[3], hi[3];
-                    float te[3];
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        lo[k] = max(mm[k] - rr, 0) << ms;
-                        hi[k] = min(mm[k] + rr + 1, mn) << ms;
-                        te[k] = ((float)((r.dg[k] >= 0.f) ? hi[k] : lo[k]) - r.o[k]) * r.inv[k];
-                    }
-                    const float texit = fminf(fminf(te[0], te[1]), te[2]);
-                    const int ax = (te[0] == texit) ? 0 : ((te[1] == texit) ? 1 : 2);
-                    if (!(texit < r.tfar)) return;
-                    t = texit;
-                    int nc[3];
-                    bool out = false;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        const float p = fmaf(t, r.dg[k], r.o[k]);
-                        const float f = floorf(p);
-                        const int ck = (int)f - (int)((r.dg[k] < 0.f) & (f == p));
-                        const int nex = (r.dg[k] > 0.f) ? hi[k] : lo[k] - 1;
-                        nc[k] = (k == ax) ? nex : min(max(ck, lo[k]), hi[k] - 1);
-                        out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
-                    }
-                    if (out) return;
-                    const int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
-                    // the stack is only valid down to the current restart level L
-                    L = min(L, D - 1 - (31 - __clz(diff)));
-                    c[0] = nc[0];
-                    c[1] = nc[1];
-                    c[2] = nc[2];
-                    continue;
-                }
-                check_macro = false;   // occupied level-M cell: plain traversal until we leave it
-            }
-        }
-        // stk[L] holds the device entry word of the node at level L; with occupancy masks the
-        // word carries the node's 8-bit child mask, so an empty octant is known without a load
+        // stk[L] holds the entry word of the node at level L (the deepest common ancestor of
+        // the previous and the current cell); descend to the box that contains cell c
         uint32_t ent = stk[L];
         uint32_t e;
         int shift;
         while (true) {
-            if constexpr (kBricks) {
-                if (L == Lb) {   // one brick load replaces the last two descent levels
-                    e = __ldg(tr.brick + (size_t)(ent & tr.node_idx_mask) * 64u +
-                              (((c[0] & 3) << 4) | ((c[1] & 3) << 2) | (c[2] & 3)));
-                    shift = 0;
-                    if ((e >> 30) == 3u) {   // a whole level-(D-1) box: empty, or one coarser leaf
-                        shift = 1;
-                        e = (e & kBrickLeafBit) ? ((kTagLeaf << 30) | (e & (kBrickLeafBit - 1u))) : 0u;
-                    }
-                    break;
-                }
-            }
             shift = D - 1 - L;
             const int oct = (((c[0] >> shift) & 1) << 2) | (((c[1] >> shift) & 1) << 1) | ((c[2] >> shift) & 1);
-            if constexpr ((OPT & kOptNodeMask) != 0) {
-                const uint32_t m = tr.node_masks ? (ent >> kMaskShift) : 0xFFu;
-                if (!((m >> oct) & 1u)) {
-                    e = 0u;   // empty octant, known from the parent's entry word
-                    break;
-                }
-            }
-            e = __ldg(child + ((ent & tr.node_idx_mask) * 8u + (uint32_t)oct));
+            e = __ldg(tr.child + ((ent & kIdxMask) * 8u + (uint32_t)oct));
             if ((e >> 30) != kTagInternal) break;
             ent = e;
             ++L;
@@ -279,10 +187,10 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         int nc[3];
         bool out = false;
         if constexpr ((OPT & kOptLean) != 0) {
-            // leaner step: every axis whose face is crossed at texit steps (an exact edge or
-            // corner crossing moves diagonally), the others are point-located with one F2I.FLOOR
-            // (an exactly integral coordinate while moving down yields a zero-length box that
-            // the `tout > t` test skips) and clamped into the box
+            // every axis whose face is crossed at texit steps (an exact edge or corner crossing
+            // moves diagonally), the others are point-located with one F2I.FLOOR (an exactly
+            // integral coordinate while moving down yields a zero-length box that the
+            // `tout > t` test skips) and clamped into the box
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const bool hit = te[k] == texit;
@@ -290,14 +198,6 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
                 const int ck = __float2int_rd(fmaf(t, r.dg[k], r.o[k]));
                 nc[k] = hit ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
                 out |= hit & ((unsigned)nex >= (unsigned)G);
-            }
-        } else if ((OPT & kOptLeafStep) && size == 1) {
-            // leaf-level box (the common step): the other two coordinates cannot change
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const int nex = c[k] + ((r.dg[k] > 0.f) ? 1 : -1);
-                nc[k] = (k == ax) ? nex : c[k];
-                out |= (k == ax) & ((unsigned)nex >= (unsigned)G);
             }
         } else {
 #pragma unroll
@@ -313,13 +213,10 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         }
         if (out) return;
         const int diff = (c[0] ^ nc[0]) | (c[1] ^ nc[1]) | (c[2] ^ nc[2]);
-        L = D - 1 - (31 - __clz(diff));
-        if constexpr (kBricks) L = min(L, Lb);   // no nodes below the brick owner
+        L = D - 1 - (31 - __clz(diff));   // restart at the deepest common ancestor
         c[0] = nc[0];
         c[1] = nc[1];
         c[2] = nc[2];
-        if constexpr ((OPT & kOptMacroSkip) != 0)
-            check_macro = tr.macro != nullptr && (diff >> tr.macro_shift) != 0;   // entered a new level-M cell
     }
 }
 
