@@ -221,6 +221,21 @@ po_status po_render_backward_chunk(const po_tree* tree, const float* rays, const
                                    const double* aux, const po_segments* segments, const po_render_opts* opts,
                                    float* grad_sigma, float* grad_sh, po_stream stream);
 
+/* Deterministic pass 2 (NEXT f2 "deterministic-reduction mode"): the same gradients as
+ * po_render_backward with stored segments, accumulated by a segmented reduction instead of
+ * atomics -- every segment's contribution is emitted with its leaf as key, the records are
+ * sorted by leaf (stable: ray order, then segment order) and each leaf's run is summed in that
+ * fixed order and added once -- so repeated calls give bit-identical gradients (the atomic path
+ * is order-nondeterministic, reading Q24).  Needs aux and segments from the same
+ * po_render_rays call.  Rays whose segments overflowed max_seg still go through the atomic
+ * re-traversal; n_overflow (device int32 or NULL) receives their number, and the result is
+ * order-fixed iff it is 0.  Synchronises the stream once (the segment total sizes the sort);
+ * scratch (~36 B per segment) is cached in the tree, so calls on one tree must not overlap. */
+po_status po_render_backward_deterministic(const po_tree* tree, const float* rays, int64_t n, const float* dL_dC,
+                                           const double* aux, const po_segments* segments,
+                                           const po_render_opts* opts, float* grad_sigma, float* grad_sh,
+                                           int32_t* n_overflow, po_stream stream);
+
 /* Eq. (3) helper: dL_dC[i] = 2 (pred[i] - target[i]) over n*3 floats; if loss != NULL,
  * *loss (device double) = sum (pred - target)^2 (overwritten). */
 po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, float* dL_dC, double* loss,

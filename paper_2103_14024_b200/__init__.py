@@ -26,7 +26,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
            "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis",
            "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
-           "po_render_backward", "po_backward_plan", "po_render_backward_chunk",
+           "po_render_backward", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
            "po_render_timeline"]
 
@@ -101,6 +101,7 @@ def lib():
         L.po_render_depth.argtypes = [P, P, I64, P, P, P, P]
         L.po_leaf_max_alpha.argtypes = [P, P, I64, P, P, P]
         L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P, P]
+        L.po_render_backward_deterministic.argtypes = [P, P, I64, P, P, P, P, P, P, P, P]
         L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
         L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
         L.po_tree_sgd_step_range.argtypes = [P, P, P, F, I64, I64, I32, P]
@@ -387,6 +388,23 @@ def po_leaf_max_alpha(tree: PlenOctree, rays, max_alpha=None, gamma: float = 0.0
     _check(lib().po_leaf_max_alpha(tree.handle, _ptr(rays), rays.shape[0], ctypes.byref(o), _ptr(max_alpha),
                                    _stream(stream)))
     return max_alpha
+
+
+def po_render_backward_deterministic(tree: PlenOctree, rays, dL_dC, grad_sigma, grad_sh, aux, segments,
+                                     gamma: float = 0.0, background=(1.0, 1.0, 1.0), n_overflow=None, stream=None):
+    """Order-fixed (bit-reproducible) pass 2 from stored segments; accumulates (+=)."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    _need(dL_dC, torch.float32, (3,))
+    _need(grad_sigma, torch.float32)
+    _need(grad_sh, torch.float32, (tree.B, 3))
+    _need(aux, torch.float64, (4,))
+    if n_overflow is not None:
+        _need(n_overflow, torch.int32)
+    o = _opts(gamma, background)
+    _check(lib().po_render_backward_deterministic(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux),
+                                                  _seg(segments), ctypes.byref(o), _ptr(grad_sigma), _ptr(grad_sh),
+                                                  _ptr(n_overflow), _stream(stream)))
 
 
 def po_l2_loss_grad(pred, target, dL_dC=None, loss=None, stream=None):

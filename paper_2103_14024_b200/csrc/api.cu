@@ -1,6 +1,7 @@
 // C-ABI layer of libplenoct (include/plenoct.h): argument validation, tree upload (a0),
 // device selection and kernel launches.  No compute happens here; there is no CPU path.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -45,6 +46,10 @@ struct po_tree {
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
     float4* d_sg = nullptr;          // spherical-Gaussian lobes (po_tree_set_sg_basis) or null
     std::vector<float> h_sg;         // the same on the host, [B][4]
+    // po_render_backward_deterministic scratch, grown on demand
+    void* d_det = nullptr;
+    size_t det_cap = 0;
+    std::mutex det_mu;
     // po_backward_plan scratch (sort keys/values + CUB temp), grown on demand
     void* d_plan = nullptr;
     size_t plan_cap = 0;
@@ -390,6 +395,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_img) cudaFree(t->d_img);
     if (t->d_order) cudaFree(t->d_order);
     if (t->d_plan) cudaFree(t->d_plan);
+    if (t->d_det) cudaFree(t->d_det);
     if (t->d_sg) cudaFree(t->d_sg);
     t->d_child = nullptr;
     delete t;
@@ -629,6 +635,7 @@ po_status po_backward_plan(po_tree* t, const uint32_t* leaf_span, int64_t n, int
     std::lock_guard<std::mutex> lk(t->plan_mu);
     if (t->plan_cap < need) {
         if (t->d_plan) cudaFree(t->d_plan);
+    if (t->d_det) cudaFree(t->d_det);
     if (t->d_sg) cudaFree(t->d_sg);
         t->d_plan = nullptr;
         t->plan_cap = 0;
@@ -691,6 +698,102 @@ po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, con
     return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
                                         sg, o, grad_sigma, grad_sh, (cudaStream_t)stream),
                     "po_render_backward");
+}
+
+static cudaError_t grow(void** p, size_t* cap, size_t need) {
+    if (*cap >= need) return cudaSuccess;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e == cudaSuccess) *cap = need;
+    return e;
+}
+
+po_status po_render_backward_deterministic(const po_tree* tc, const float* rays, int64_t n, const float* dL_dC,
+                                           const double* aux, const po_segments* segments, const po_render_opts* opts,
+                                           float* grad_sigma, float* grad_sh, int32_t* n_overflow, po_stream stream) {
+    po_tree* t = const_cast<po_tree*>(tc);   // scratch only
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (n < 0 || n >= (int64_t)INT32_MAX) return fail(PO_ERR_INVALID_ARG, "n outside [0, 2^31 - 1)");
+    if (!segments || !aux) return fail(PO_ERR_INVALID_ARG, "the deterministic backward needs segments and aux");
+    po::Segments sg;
+    if (po_status s = check_segments(segments, n, aux, &sg)) return s;
+    if (!rays || !dL_dC || !grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
+    if (n * (int64_t)std::max(segments->max_seg, 1) >= (int64_t)INT32_MAX)
+        return fail(PO_ERR_UNSUPPORTED, "n * max_seg >= 2^31 (32-bit segment slots)");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (n_overflow && (e = cudaMemsetAsync(n_overflow, 0, sizeof(int32_t), s)) != cudaSuccess)
+        return cuda_status(e, "memset(n_overflow)");
+    if (n == 0) return PO_OK;
+    std::lock_guard<std::mutex> lk(t->det_mu);
+    const po::DevTree dt = dev_tree(t);
+    // 1-2: per-ray emitted counts and their exclusive scan (one host sync reads the total S)
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(n + 1), s);
+    scan_bytes = (scan_bytes + 255) / 256 * 256;   // keeps the records after it 16-B aligned
+    const size_t a1 = ((size_t)(n + 1) * 4 + 255) / 256 * 256;
+    if ((e = grow(&t->d_det, &t->det_cap, 2 * a1 + scan_bytes)) != cudaSuccess) return cuda_status(e, "scratch");
+    int32_t* cnt = static_cast<int32_t*>(t->d_det);
+    int32_t* offs = reinterpret_cast<int32_t*>(static_cast<char*>(t->d_det) + a1);
+    if ((e = po::launch_det_counts(rays, n, dL_dC, sg, cnt, n_overflow, s)) != cudaSuccess) return cuda_status(e, "counts");
+    if ((e = cub::DeviceScan::ExclusiveSum(static_cast<char*>(t->d_det) + 2 * a1, scan_bytes, cnt, offs, (int)(n + 1),
+                                           s)) != cudaSuccess)
+        return cuda_status(e, "scan");
+    int32_t S32 = 0;
+    if ((e = cudaMemcpyAsync(&S32, offs + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        return cuda_status(e, "segment total");
+    const int64_t S = S32;
+    // 3-5: emit, sort by leaf, reduce per leaf in slot order
+    int end_bit = 1;
+    while (end_bit < 32 && ((uint64_t)1 << end_bit) <= (uint64_t)t->n_leaves) ++end_bit;
+    size_t sort_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)std::max<int64_t>(S, 1), 0,
+                                    end_bit, s);
+    const size_t a4 = ((size_t)std::max<int64_t>(S, 1) * 4 + 255) / 256 * 256;
+    const size_t need = 2 * a1 + scan_bytes + 5 * a4 + 4 * a4 + sort_bytes;
+    if (t->det_cap < need) {   // keep cnt / offs: grow into a fresh block and copy offs over
+        void* nb = nullptr;
+        if ((e = cudaMalloc(&nb, need)) != cudaSuccess) return cuda_status(e, "scratch");
+        e = cudaMemcpyAsync(static_cast<char*>(nb) + a1, offs, (size_t)(n + 1) * 4, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(t->d_det);
+        t->d_det = nb;
+        t->det_cap = need;
+        if (e != cudaSuccess) return cuda_status(e, "scratch copy");
+        offs = reinterpret_cast<int32_t*>(static_cast<char*>(t->d_det) + a1);
+    }
+    char* b = static_cast<char*>(t->d_det) + 2 * a1 + scan_bytes;
+    uint32_t* key = reinterpret_cast<uint32_t*>(b);
+    uint32_t* val = reinterpret_cast<uint32_t*>(b + a4);
+    uint32_t* skey = reinterpret_cast<uint32_t*>(b + 2 * a4);
+    uint32_t* sval = reinterpret_cast<uint32_t*>(b + 3 * a4);
+    int32_t* ray_of = reinterpret_cast<int32_t*>(b + 4 * a4);
+    float4* contrib = reinterpret_cast<float4*>(b + 5 * a4);
+    void* sort_tmp = b + 9 * a4;
+    if ((e = po::launch_det_emit(dt, t->desc.sh_degree, rays, n, dL_dC, aux, sg, offs, key, val, contrib, ray_of, s)) !=
+        cudaSuccess)
+        return cuda_status(e, "emit");
+    if (S > 0 &&
+        (e = cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, key, skey, val, sval, (int)S, 0, end_bit, s)) !=
+            cudaSuccess)
+        return cuda_status(e, "sort");
+    if ((e = po::launch_det_reduce(dt, t->desc.sh_degree, rays, skey, sval, S, contrib, ray_of, grad_sigma, grad_sh,
+                                   s)) != cudaSuccess)
+        return cuda_status(e, "reduce");
+    g_launches.fetch_add(3);   // counts, emit, reduce (+ CUB's scan / sort kernels, library code)
+    // rays whose segments overflowed max_seg: the re-traversal (atomic, not order-fixed)
+    return launched(po::launch_backward(dt, t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux, sg, o,
+                                        grad_sigma, grad_sh, s, true),
+                    "po_render_backward_deterministic");
 }
 
 po_status po_l2_loss_grad(const float* pred, const float* target, int64_t n, float* dL_dC, double* loss,

@@ -568,13 +568,54 @@ __global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __
 // across 32-segment rounds (same sum as the sequential pass up to double rounding order);
 // then every lane applies GradVisitor::seg's formula to its own segment.  Rays whose segments
 // overflowed (count > max_seg) are left to k_backward<..., true>.
+// Where the replay puts each segment's gradient: atomically into the leaf rows (default), or as
+// a record for the deterministic segmented reduction (po_render_backward_deterministic).
 template <int DEG>
+struct AtomicSink {
+    float* __restrict__ grad_sigma;
+    float* __restrict__ grad_sh;
+    __device__ __forceinline__ void operator()(int32_t, uint32_t idx, float gsig, const float gz[3], const float* Y) {
+        constexpr int NE = 3 * ShDim<DEG>::B;
+        atomicAdd(grad_sigma + idx, gsig);
+        float* row = grad_sh + (size_t)idx * NE;
+        if constexpr (NE % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < NE / 4; ++j) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3];
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * j), "f"(v[0]),
+                             "f"(v[1]), "f"(v[2]), "f"(v[3])
+                             : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int el = 0; el < NE; ++el) atomicAdd(row + el, gz[el % 3] * Y[el / 3]);
+        }
+    }
+};
+
+struct EmitSink {   // segment k of ray `ray` -> flat slot f0 + k
+    uint32_t* __restrict__ key;
+    uint32_t* __restrict__ val;
+    float4* __restrict__ contrib;
+    int32_t* __restrict__ ray_of;
+    int64_t f0;
+    int32_t ray;
+    __device__ __forceinline__ void operator()(int32_t k, uint32_t idx, float gsig, const float gz[3], const float*) {
+        const int64_t f = f0 + k;
+        key[f] = idx;
+        val[f] = (uint32_t)f;
+        contrib[f] = make_float4(gsig, gz[0], gz[1], gz[2]);
+        ray_of[f] = ray;
+    }
+};
+
+template <int DEG, class Sink>
 __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __restrict__ rays, int64_t i,
                                            const float* __restrict__ dL_dC, const double* __restrict__ aux,
-                                           const SegIn& si, float* __restrict__ grad_sigma,
-                                           float* __restrict__ grad_sh) {
+                                           const SegIn& si, Sink& sink) {
     constexpr int B = ShDim<DEG>::B;
-    constexpr int NE = 3 * B;
     const int lane = threadIdx.x & 31;
     const int32_t ns = __ldg(si.count + i);
     if (ns == 0 || ns > si.max_seg) return;
@@ -618,25 +659,10 @@ __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __res
         double acc = 0.0;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) acc += (double)g[ch] * ((double)c[ch] * (double)Tn - (Ctot[ch] - P[ch]));
-        atomicAdd(grad_sigma + idx, (float)((double)delta * acc));
         float gz[3];
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) gz[ch] = g[ch] * w * c[ch] * (1.f - c[ch]);
-        float* row = grad_sh + (size_t)idx * NE;
-        if constexpr (NE % 4 == 0) {
-#pragma unroll
-            for (int j = 0; j < NE / 4; ++j) {
-                float v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3];
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * j), "f"(v[0]),
-                             "f"(v[1]), "f"(v[2]), "f"(v[3])
-                             : "memory");
-            }
-        } else {
-#pragma unroll
-            for (int el = 0; el < NE; ++el) atomicAdd(row + el, gz[el % 3] * Y[el / 3]);
-        }
+        sink(k, idx, (float)((double)delta * acc), gz, Y);
     }
 }
 
@@ -648,7 +674,8 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const fl
                                                          float* __restrict__ grad_sh) {
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= n) return;
-    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, grad_sigma, grad_sh);
+    AtomicSink<DEG> sink{grad_sigma, grad_sh};
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
 }
 
 // the same over one chunk of a po_backward_plan (bounds on the device): a persistent grid
@@ -665,8 +692,86 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay_chunk(DevTree tr, co
     const int64_t b = chunk > 0 ? chunk_end[chunk - 1] : 0, e = chunk_end[chunk];
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t j = b + w0; j < e; j += nw)
-        replay_ray<DEG>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, grad_sigma, grad_sh);
+    AtomicSink<DEG> sink{grad_sigma, grad_sh};
+    for (int64_t j = b + w0; j < e; j += nw) replay_ray<DEG>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, sink);
+}
+
+// ---- deterministic pass 2: segmented reduction into leaves (NEXT f2 "deterministic-reduction
+// mode"; the north star's alternative to atomics).  1) per ray, the number of segments it will
+// emit (0 where the atomic replay would return early; overflow rays are counted and left to
+// the re-traversal); 2) exclusive scan -> flat slots; 3) the replay emits (leaf, slot) keys and
+// (dL/dsigma~, gz) records; 4) stable radix sort by leaf; 5) one thread per leaf sums its run in
+// slot order (= ray order, then k) and adds the sums once: every float sum has a fixed order.
+__global__ void __launch_bounds__(256) k_det_counts(const float* __restrict__ rays, int64_t n,
+                                                    const float* __restrict__ dL_dC, SegIn si,
+                                                    int32_t* __restrict__ cnt, int32_t* __restrict__ n_overflow) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == n) {   // trailing 0: the exclusive scan then ends with the total
+        cnt[i] = 0;
+        return;
+    }
+    const int32_t ns = __ldg(si.count + i);
+    int32_t c = ns;
+    if (ns > si.max_seg) {
+        c = 0;
+        if (n_overflow) atomicAdd(n_overflow, 1);
+    } else if (ns > 0) {
+        float dir[3], d[3];
+        const float g0 = __ldg(dL_dC + i * 3), g1 = __ldg(dL_dC + i * 3 + 1), g2 = __ldg(dL_dC + i * 3 + 2);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dir[k] = __ldg(rays + i * 6 + 3 + k);
+        if ((g0 == 0.f && g1 == 0.f && g2 == 0.f) || !unit_direction(dir, d)) c = 0;
+    }
+    cnt[i] = c;
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(256, 3) k_det_emit(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                  const float* __restrict__ dL_dC, const double* __restrict__ aux,
+                                                  SegIn si, const int32_t* __restrict__ offs,
+                                                  uint32_t* __restrict__ key, uint32_t* __restrict__ val,
+                                                  float4* __restrict__ contrib, int32_t* __restrict__ ray_of) {
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= n) return;
+    EmitSink sink{key, val, contrib, ray_of, (int64_t)__ldg(offs + i), (int32_t)i};
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(256) k_det_reduce(DevTree tr, const float* __restrict__ rays,
+                                                    const uint32_t* __restrict__ skey,
+                                                    const uint32_t* __restrict__ sval, int64_t S,
+                                                    const float4* __restrict__ contrib,
+                                                    const int32_t* __restrict__ ray_of, float* __restrict__ grad_sigma,
+                                                    float* __restrict__ grad_sh) {
+    constexpr int B = ShDim<DEG>::B;
+    constexpr int NE = 3 * B;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S) return;
+    const uint32_t leaf = skey[j];
+    if (j > 0 && skey[j - 1] == leaf) return;   // one thread per run of equal leaves
+    float ss = 0.f, acc[NE];
+#pragma unroll
+    for (int el = 0; el < NE; ++el) acc[el] = 0.f;
+    for (int64_t m = j; m < S && skey[m] == leaf; ++m) {
+        const uint32_t f = sval[m];
+        const float4 c4 = contrib[f];
+        const int32_t r = ray_of[f];
+        float dir[3], d[3], Y[B];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dir[k] = __ldg(rays + (int64_t)r * 6 + 3 + k);
+        unit_direction(dir, d);
+        ray_basis<DEG>(tr, d, Y);
+        const float gz[3] = {c4.y, c4.z, c4.w};
+        ss += c4.x;
+#pragma unroll
+        for (int el = 0; el < NE; ++el) acc[el] += gz[el % 3] * Y[el / 3];
+    }
+    grad_sigma[leaf] += ss;
+    float* row = grad_sh + (size_t)leaf * NE;
+#pragma unroll
+    for (int el = 0; el < NE; ++el) row[el] += acc[el];
 }
 
 // Pass 2 over one chunk of a po_backward_plan: rays perm[chunk_end[c-1] .. chunk_end[c]).
@@ -1059,6 +1164,35 @@ cudaError_t launch_backward_chunk(const DevTree& tr, int deg, bool f16, const fl
     return cudaGetLastError();
 }
 
+cudaError_t launch_det_counts(const float* rays, int64_t n, const float* dL_dC, const Segments& sg, int32_t* cnt,
+                              int32_t* n_overflow, cudaStream_t s) {
+    const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+    k_det_counts<<<grid1d(n + 1, 256), 256, 0, s>>>(rays, n, dL_dC, si, cnt, n_overflow);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_det_emit(const DevTree& tr, int deg, const float* rays, int64_t n, const float* dL_dC,
+                            const double* aux, const Segments& sg, const int32_t* offs, uint32_t* key, uint32_t* val,
+                            float4* contrib, int32_t* ray_of, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+    PO_DISPATCH(deg, false, {
+        k_det_emit<DEG><<<grid1d(n, 8), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, offs, key, val, contrib, ray_of);
+    });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_det_reduce(const DevTree& tr, int deg, const float* rays, const uint32_t* skey,
+                              const uint32_t* sval, int64_t S, const float4* contrib, const int32_t* ray_of,
+                              float* grad_sigma, float* grad_sh, cudaStream_t s) {
+    if (S == 0) return cudaSuccess;
+    PO_DISPATCH(deg, false, {
+        k_det_reduce<DEG><<<grid1d(S, 256), 256, 0, s>>>(tr, rays, skey, sval, S, contrib, ray_of, grad_sigma,
+                                                         grad_sh);
+    });
+    return cudaGetLastError();
+}
+
 cudaError_t launch_plan_keys(const uint32_t* span, int64_t n, uint32_t n_leaves, uint32_t* keys, int32_t* idx,
                              cudaStream_t s) {
     if (n == 0) return cudaSuccess;
@@ -1074,14 +1208,15 @@ cudaError_t launch_plan_ends(const uint32_t* sorted_keys, int64_t n, int64_t n_l
 
 cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
                             const double* aux, const Segments& sg, const RenderOpts& opt, float* grad_sigma,
-                            float* grad_sh, cudaStream_t s) {
+                            float* grad_sh, cudaStream_t s, bool overflow_only) {
     if (n == 0) return cudaSuccess;
     const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
     const bool replay = aux != nullptr && sg.count != nullptr;
     PO_DISPATCH(deg, f16, {
         if (replay) {   // stored segments first, then the overflow rays by re-traversal
             carveout_once(k_backward_replay<DEG>);
-            k_backward_replay<DEG><<<grid1d(n, 8), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, grad_sigma, grad_sh);
+            if (!overflow_only)
+                k_backward_replay<DEG><<<grid1d(n, 8), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, grad_sigma, grad_sh);
             carveout_once(k_backward<DEG, F16, true>);
             k_backward<DEG, F16, true><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, opt, grad_sigma,
                                                                       grad_sh);

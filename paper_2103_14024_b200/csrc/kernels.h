@@ -36,6 +36,14 @@ cudaError_t launch_backward_chunk(const DevTree& tr, int deg, bool f16, const fl
                                   const int64_t* chunk_end, int chunk, const float* dL_dC, const double* aux,
                                   const Segments& sg, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
                                   unsigned* work, cudaStream_t s);
+cudaError_t launch_det_counts(const float* rays, int64_t n, const float* dL_dC, const Segments& sg, int32_t* cnt,
+                              int32_t* n_overflow, cudaStream_t s);
+cudaError_t launch_det_emit(const DevTree& tr, int deg, const float* rays, int64_t n, const float* dL_dC,
+                            const double* aux, const Segments& sg, const int32_t* offs, uint32_t* key, uint32_t* val,
+                            float4* contrib, int32_t* ray_of, cudaStream_t s);
+cudaError_t launch_det_reduce(const DevTree& tr, int deg, const float* rays, const uint32_t* skey,
+                              const uint32_t* sval, int64_t S, const float4* contrib, const int32_t* ray_of,
+                              float* grad_sigma, float* grad_sh, cudaStream_t s);
 cudaError_t launch_plan_keys(const uint32_t* span, int64_t n, uint32_t n_leaves, uint32_t* keys, int32_t* idx,
                              cudaStream_t s);
 constexpr int kMaxPlanChunks = 64;
@@ -45,9 +53,10 @@ struct PlanBounds {
 };
 cudaError_t launch_plan_ends(const uint32_t* sorted_keys, int64_t n, int64_t n_leaves, const PlanBounds& b,
                              int64_t* chunk_end, int64_t* quant, cudaStream_t s);
+// overflow_only (with segments): skip the replay, re-traverse only the rays that overflowed
 cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
                             const double* aux, const Segments& sg, const RenderOpts& opt, float* grad_sigma,
-                            float* grad_sh, cudaStream_t s);
+                            float* grad_sh, cudaStream_t s, bool overflow_only = false);
 cudaError_t launch_render_depth(const DevTree& tr, const float* rays, int64_t n, float gamma, float* alpha,
                                 float* depth, cudaStream_t s);
 cudaError_t launch_leaf_max_alpha(const DevTree& tr, const float* rays, int64_t n, float gamma, float* max_alpha,

@@ -22,14 +22,16 @@ from __future__ import annotations
 
 import torch
 
-from . import (Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk, po_render_rays,
+from . import (Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk,
+               po_render_backward_deterministic, po_render_rays,
                po_tree_sgd_step_range)
 from .dist import agree_bounds, allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets
 
 
 class OctreeOptimizer:
     def __init__(self, tree, lr: float, gamma: float = 0.0, background=(1.0, 1.0, 1.0), group=None,
-                 bucket_mb: float = 64.0, device=None, chunks=None, max_seg: int = 256):
+                 bucket_mb: float = 64.0, device=None, chunks=None, max_seg: int = 256,
+                 deterministic: bool = False):
         self.tree = tree
         self.lr = float(lr)
         self.gamma = float(gamma)
@@ -50,6 +52,10 @@ class OctreeOptimizer:
         self.leaf_bounds = {}   # K -> host leaf bounds of po_backward_plan (calibrated on first use)
         # stored pass-1 segments per ray (po_segments, max_seg * n * 32 B); 0 = re-traverse in pass 2
         self.max_seg = int(max_seg)
+        # order-fixed pass 2 (po_render_backward_deterministic): bit-reproducible gradients
+        self.deterministic = bool(deterministic)
+        if self.deterministic and self.max_seg <= 0:
+            raise ValueError("the deterministic backward replays stored segments: max_seg must be > 0")
 
     @property
     def world_size(self) -> int:
@@ -82,6 +88,8 @@ class OctreeOptimizer:
         # the gradient buffer is zero here: it starts zeroed and every SGD call below zeroes
         # what it consumed (PO_SGD_ZERO_GRAD), which replaces a 0.7 GB memset per step
         nl = self.tree.n_leaves
+        if K > 1 and self.deterministic:
+            raise ValueError("deterministic pass 2 is not combined with the chunked overlap")
         if K > 1:
             key = ("plan", K)
             if key not in self._bufs:
@@ -122,8 +130,12 @@ class OctreeOptimizer:
             overlapped_chunks(self.flat, leaf_end, nl, self.tree.B, self.sh_off, run_chunk, apply_final,
                               group=self.group, world_size=self.world_size)
             return self.loss
-        po_render_backward(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux=aux, gamma=self.gamma,
-                           background=self.background, segments=seg)
+        if self.deterministic:
+            po_render_backward_deterministic(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux, seg,
+                                             gamma=self.gamma, background=self.background)
+        else:
+            po_render_backward(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux=aux, gamma=self.gamma,
+                               background=self.background, segments=seg)
         if self.world_size > 1:
             works = allreduce_buckets(self.flat, self.buckets, self.group)
             for (s, e), w in zip(self.buckets, works):

@@ -352,6 +352,40 @@ def test_backward_plan_exact(env):
         po.po_backward_plan(tree, span, 65)
 
 
+@pytest.mark.parametrize("deg,max_seg,gamma", [(1, 64, 0.0), (3, 64, 0.0), (3, 64, 0.01), (3, 3, 0.0), (4, 64, 0.0)])
+def test_deterministic_backward(env, deg, max_seg, gamma):
+    """po_render_backward_deterministic: the oracle's gradient (same bars as the atomic path),
+    bit-identical on repeated calls when no ray overflows max_seg, overflow rays counted and
+    still correct (they go through the atomic re-traversal)."""
+    po, om, torch = env
+    t = gen.scene_random(90 + deg, depth=5, sh_degree=deg, sigma_scale=3.0)
+    rays = gen.random_rays(91, 3000, inside_frac=0.1)
+    ot = om.OracleTree(t)
+    ok = _tie_free(om, ot, rays.astype(np.float64), gamma if gamma > 0 else 1e-30)
+    rays = rays[ok]
+    n = rays.shape[0]
+    tree = po.tree_from_gen(t)
+    r = _dev(torch, rays)
+    g = _dev(torch, rng(92).normal(size=(n, 3)).astype(np.float32))
+    aux = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+    seg = po.Segments(n, max_seg)
+    po.po_render_rays(tree, r, aux=aux, gamma=gamma, segments=seg)
+    outs = []
+    for _ in range(2):
+        gs = torch.zeros(tree.n_leaves, device="cuda")
+        gk = torch.zeros((tree.n_leaves, tree.B, 3), device="cuda")
+        nov = torch.zeros(1, dtype=torch.int32, device="cuda")
+        po.po_render_backward_deterministic(tree, r, g, gs, gk, aux, seg, gamma=gamma, n_overflow=nov)
+        outs.append((gs.cpu().numpy(), gk.cpu().numpy(), int(nov.item())))
+    want_over = int((seg.count.cpu().numpy() > max_seg).sum())
+    assert outs[0][2] == outs[1][2] == want_over
+    if want_over == 0:
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    rs, rk = om.backward(ot, rays.astype(np.float64), g.cpu().numpy().astype(np.float64), gamma=gamma)
+    _grad_ok(outs[0][0], rs, "sigma")
+    _grad_ok(outs[0][1], rk, "sh")
+
+
 @pytest.mark.parametrize("seed,deg,max_seg", [(31, 1, None), (32, 2, None), (33, 3, None), (34, 0, None),
                                               (35, 3, 8), (36, 1, 8), (37, 4, None), (38, 4, 8)])
 def test_random_tree_backward(env, seed, deg, max_seg):
