@@ -34,6 +34,8 @@ for ms in (64, 2):
     o2.step(rays, out)
     o3 = OctreeOptimizer(tree, lr=1.0, max_seg=ms, chunks=1)
     o3.step(rays, out)
+o4 = OctreeOptimizer(tree, lr=1.0, max_seg=2, deterministic=True)   # segmented reduction + overflow
+o4.step(rays, out)
 # NEXT rows: depth / alpha, max alpha, SH-25, SG basis, fp16 export, leaf write
 po.po_render_depth(tree, rays)
 po.po_leaf_max_alpha(tree, rays)
