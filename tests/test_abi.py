@@ -88,3 +88,14 @@ def test_rejects_bad_args_without_gpu(po):
     # chunk plan: NULL tree, bad K
     assert po.lib().po_backward_plan(None, None, 1, 4, None, None, None, None, None, None) == 1
     assert po.lib().po_render_backward_chunk(None, None, None, None, 0, None, None, None, None, None, None, None) == 1
+    # NULL tree handles are rejected before any device work, by every entry point
+    L = po.lib()
+    assert L.po_render_backward_deterministic(None, None, 1, None, None, None, ctypes.byref(o), None, None, None,
+                                              None) == 1
+    assert L.po_render_depth(None, None, 1, ctypes.byref(o), None, None, None) == 1
+    assert L.po_leaf_max_alpha(None, None, 1, ctypes.byref(o), None, None) == 1
+    assert L.po_tree_set_sg_basis(None, None, None) == 1
+    assert L.po_tree_write_leaves(None, None, None) == 1
+    h = ctypes.c_void_p()
+    assert L.po_tree_convert(None, 1, ctypes.byref(h)) == 1 and h.value is None
+    assert L.po_tree_sgd_step_range(None, None, None, ctypes.c_float(1.0), 0, 1, 0, None) == 1
