@@ -42,5 +42,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "render_uniform.c")
+EXAMPLE_BIN = os.path.join(ROOT, "examples", "render_uniform")
+
+
+def build_example() -> str:
+    """The plain-C example against include/plenoct.h + libplenoct.so (no CUDA headers)."""
+    lib = build()
+    if os.path.exists(EXAMPLE_BIN) and os.path.getmtime(EXAMPLE_BIN) >= max(os.path.getmtime(EXAMPLE_SRC),
+                                                                         os.path.getmtime(lib)):
+        return EXAMPLE_BIN
+    cmd = ["gcc", "-O2", "-Wall", "-Wextra", "-Werror", EXAMPLE_SRC, "-I", os.path.join(ROOT, "include"), "-L", PKG,
+           "-lplenoct", "-Wl,-rpath,$ORIGIN/../paper_2103_14024_b200", "-lm", "-o", EXAMPLE_BIN]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("gcc failed on the C example:\n" + res.stdout + res.stderr)
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

@@ -99,3 +99,10 @@ def test_rejects_bad_args_without_gpu(po):
     h = ctypes.c_void_p()
     assert L.po_tree_convert(None, 1, ctypes.byref(h)) == 1 and h.value is None
     assert L.po_tree_sgd_step_range(None, None, None, ctypes.c_float(1.0), 0, 1, 0, None) == 1
+
+
+def test_c_example_builds(po):
+    """examples/render_uniform.c compiles with -Werror against include/plenoct.h alone and links
+    libplenoct.so: the boundary needs no CUDA or torch headers (it runs under -m gpu)."""
+    from paper_2103_14024_b200 import _build
+    assert os.path.exists(_build.build_example())
