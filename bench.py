@@ -181,8 +181,25 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    tile_shard = args.shard == "tile" and wl in ("c1", "c3")
+
     def view_of(step):   # first of the V consecutive views rank `rank` renders at `step`
-        return 0 if wl == "c2" else ((step * ws + rank) * V) % n_views
+        if wl == "c2":
+            return 0
+        if tile_shard:   # every rank renders its blocks of the SAME view
+            return (step * V) % n_views
+        return ((step * ws + rank) * V) % n_views
+
+    def render_step(v):
+        if not tile_shard:
+            po.po_render(tree, cams[v:v + V], W, H, out=out, gamma=GAMMA)
+            return
+        # single-view latency mode: interleaved 16x16 blocks per rank, then a SUM
+        # allreduce of the zero-initialised images assembles the frame on every rank
+        out.zero_()
+        po.po_render_shard(tree, cams[v:v + V], W, H, rank, ws, out=out, gamma=GAMMA)
+        if ws > 1:
+            torch.distributed.all_reduce(out, op=torch.distributed.ReduceOp.SUM)
 
     # algorithmic bytes per launch: counters of the same traversal
     B = t_gen.basis_dim
@@ -198,10 +215,12 @@ def run_ours(args):
     K = max(args.steps, 1)
     alg_bytes = ((stats["leaf_visits"] * 4 + stats["sh_rows"] * row_bytes + stats["nodes"] * 32) / K
                  + (W * H * 12 + 64) * V)
+    if args.shard == "tile" and wl in ("c1", "c3"):
+        alg_bytes /= ws   # each rank renders 1/N of the blocks (interleaved: an even share)
 
     for s in range(args.warmup):
         flush.zero_()
-        po.po_render(tree, cams[view_of(s):view_of(s) + V], W, H, out=out, gamma=GAMMA)
+        render_step(view_of(s))
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -218,7 +237,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         v = view_of(s) if args.l2 != "same" else view_of(args.warmup)
         e0.record(stream)
-        po.po_render(tree, cams[v:v + V], W, H, out=out, gamma=GAMMA)
+        render_step(v)
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
@@ -233,7 +252,7 @@ def run_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_per_step = t_max / K
-    fps = (C2_VIEWS if wl == "c2" else ws * V) * K / (t_max / 1e3)
+    fps = (C2_VIEWS if wl == "c2" else (V if tile_shard else ws * V)) * K / (t_max / 1e3)
     kernel_ms = t_ms / K   # one kernel launch per step
 
     # e2e: the same frames through the host-buffer C-ABI entry point (H2D cameras, D2H image)
@@ -246,13 +265,23 @@ def run_ours(args):
         po.po_render_host(tree, cams_pinned[view_of(s):view_of(s) + V], W, H, out_host=pinned, gamma=GAMMA)
     if ws > 1:
         torch.distributed.barrier()
+    cams_dev = torch.empty((V, 16), dtype=torch.float32, device=dev)
+    pinned_t = torch.from_numpy(pinned)
     for s in range(args.warmup, args.warmup + e2e_steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         v = view_of(s)
         e0.record(stream)
-        po.po_render_host(tree, cams_pinned[v:v + V], W, H, out_host=pinned, gamma=GAMMA)
+        if tile_shard:   # H2D cameras, this rank's blocks, allreduce, D2H of the assembled frame
+            cams_dev.copy_(torch.from_numpy(cams_pinned[v:v + V]), non_blocking=True)
+            out.zero_()
+            po.po_render_shard(tree, cams_dev, W, H, rank, ws, out=out, gamma=GAMMA)
+            if ws > 1:
+                torch.distributed.all_reduce(out, op=torch.distributed.ReduceOp.SUM)
+            pinned_t.copy_(out, non_blocking=True)
+        else:
+            po.po_render_host(tree, cams_pinned[v:v + V], W, H, out_host=pinned, gamma=GAMMA)
         e1.record(stream)
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
@@ -260,7 +289,7 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_fps = (C2_VIEWS if wl == "c2" else ws * V) * e2e_steps / (e2e_ms / 1e3)
+    e2e_fps = (C2_VIEWS if wl == "c2" else (V if tile_shard else ws * V)) * e2e_steps / (e2e_ms / 1e3)
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -269,9 +298,12 @@ def run_ours(args):
         line = {
             "metric": metric, "value": round(fps, 2), "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": "strong" if wl == "c2" else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if (wl == "c2" or tile_shard) else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (procedural SDF scene, seeded)",
-            "config": _workload_desc(t_gen, wl, ws) | {"parallelism": f"view-sharded x{ws}, tree replicated"}
+            "config": _workload_desc(t_gen, wl, ws)
+                      | {"parallelism": (f"tile-sharded x{ws} (interleaved 16x16 blocks of one view, SUM allreduce of "
+                                         "the image), tree replicated") if tile_shard
+                         else f"view-sharded x{ws}, tree replicated"}
                       | ({"global_batch": f"{V} frames per rank per step (one launch)"} if V > 1 and wl != "c2"
                          else {})
                       | ({"l2": f"NOT flushed ({args.l2}): analysis only"} if args.l2 != "flush" else {}),
@@ -291,7 +323,9 @@ def run_ours(args):
                                           "+ 12 B/pixel out",
                          "traffic_source": tsrc},
             "e2e": {"value": round(e2e_fps, 2), "unit": unit, "h2d_bytes_per_step": 64 * V,
-                    "d2h_bytes_per_step": W * H * 12 * V, "entry": "po_render_host (host cameras -> host image)"},
+                    "d2h_bytes_per_step": W * H * 12 * V,
+                    "entry": ("po_render_shard + image allreduce, cameras H2D / frame D2H" if tile_shard
+                              else "po_render_host (host cameras -> host image)")},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -530,6 +564,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4"], default="c1")
+    ap.add_argument("--shard", choices=["view", "tile"], default="view",
+                    help="c1/c3 at N>1: views per rank (weak) or the blocks of one view per rank (strong)")
     ap.add_argument("--views-per-launch", type=int, default=1,
                     help="render V consecutive orbit views per po_render launch (c2-style batches)")
     ap.add_argument("--l2", choices=["flush", "orbit", "same"], default="flush",

@@ -121,6 +121,16 @@ po_status po_tree_read_leaves(const po_tree* tree, float* sigma, float* sh);
 po_status po_render(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                     const po_render_opts* opts, float* out_rgb, po_stream stream);
 
+/* Tile sharding of one render (SURVEY 8(e) single-view latency mode): writes only the 16x16
+ * pixel blocks at hand-out positions k with k % shard_count == shard_index (the centre-out
+ * order, so every shard gets an equal mix of costly central and cheap border blocks); the
+ * other pixels of out_rgb are left untouched.  Shards 0..shard_count-1 rendered into zeroed
+ * images on as many GPUs and summed (e.g. a NCCL allreduce of the image) give exactly
+ * po_render's image.  shard_count 1..4096. */
+po_status po_render_shard(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                          const po_render_opts* opts, int32_t shard_index, int32_t shard_count, float* out_rgb,
+                          po_stream stream);
+
 /* Same as po_render with HOST cameras and a HOST output image: copies the cameras in,
  * renders, copies the image out and synchronises the stream (end-to-end entry point).  If
  * out_rgb_host is pinned (cudaHostAlloc / torch pin_memory: device-mapped under unified

@@ -25,7 +25,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
            "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis",
-           "po_tree_read_leaves", "po_render", "po_render_host", "po_camera_rays", "po_render_rays",
+           "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
            "po_render_timeline"]
@@ -93,6 +93,7 @@ def lib():
         L.po_tree_info.argtypes = [P, P, P, P]
         L.po_tree_read_leaves.argtypes = [P, P, P]
         L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
+        L.po_render_shard.argtypes = [P, P, I32, I32, I32, P, I32, I32, P, P]
         L.po_render_host.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_rays.argtypes = [P, P, I64, P, P, P, P, P, P]
         L.po_backward_plan.argtypes = [P, P, I64, I32, P, P, P, P, P, P]
@@ -252,6 +253,21 @@ def po_render(tree: PlenOctree, cams, W: int, H: int, out=None, gamma: float = 0
     _need(out, torch.float32, (H, W, 3))
     o = _opts(gamma, background)
     _check(lib().po_render(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), _ptr(out), _stream(stream)))
+    return out
+
+
+def po_render_shard(tree: PlenOctree, cams, W: int, H: int, shard_index: int, shard_count: int, out=None,
+                    gamma: float = 0.01, background=(1.0, 1.0, 1.0), stream=None):
+    """Render only this shard's 16x16 blocks of the views (others untouched; `out` zeroed if new)."""
+    import torch
+    cams = _need(cams, torch.float32, (16,))
+    n = cams.shape[0]
+    if out is None:
+        out = torch.zeros((n, H, W, 3), dtype=torch.float32, device=cams.device)
+    _need(out, torch.float32, (H, W, 3))
+    o = _opts(gamma, background)
+    _check(lib().po_render_shard(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), int(shard_index),
+                                 int(shard_count), _ptr(out), _stream(stream)))
     return out
 
 

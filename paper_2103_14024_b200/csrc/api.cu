@@ -483,6 +483,25 @@ po_status po_render(const po_tree* t, const po_camera* cams, int32_t n_cams, int
     return render_scheduled(tm, cams, n_cams, W, H, o, out_rgb, (cudaStream_t)stream, "po_render");
 }
 
+po_status po_render_shard(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
+                          const po_render_opts* opts, int32_t shard_index, int32_t shard_count, float* out_rgb,
+                          po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    if (po_status s = check_image(n_cams, W, H)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (shard_count < 1 || shard_count > 4096 || shard_index < 0 || shard_index >= shard_count)
+        return fail(PO_ERR_INVALID_ARG, "need 0 <= shard_index < shard_count <= 4096");
+    if (n_cams == 0) return PO_OK;
+    if (!cams || !out_rgb) return fail(PO_ERR_INVALID_ARG, "cams / out_rgb NULL");
+    o.shard_index = shard_index;
+    o.shard_count = shard_count;
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    po_tree* tm = const_cast<po_tree*>(t);
+    return render_scheduled(tm, cams, n_cams, W, H, o, out_rgb, (cudaStream_t)stream, "po_render_shard");
+}
+
 po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
                          const po_render_opts* opts, float* out_host, po_stream stream) {
     po_tree* t = const_cast<po_tree*>(tc);   // only the camera scratch is mutated

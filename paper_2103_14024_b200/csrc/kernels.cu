@@ -344,7 +344,10 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
     __syncthreads();
     const unsigned bx_n = (unsigned)(W + 15) >> 4, by_n = (unsigned)(H + 15) >> 4;
     const unsigned per_view = bx_n * by_n;
-    const unsigned total = per_view * (unsigned)n_cams;
+    // blocks of this shard per view: hand-out positions k = local * shard_count + shard_index
+    const unsigned sc = (unsigned)opt.shard_count, si = (unsigned)opt.shard_index;
+    const unsigned local_per_view = (per_view + sc - 1u - si) / sc;
+    const unsigned total = local_per_view * (unsigned)n_cams;
     while (true) {
         // hand-off through shared-memory atomics (ordered by the block fences): the warp that
         // opens a slot claims the block and publishes it; the other 7 wait for the flag.  The
@@ -373,8 +376,8 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         if (lane == 0) blk = atomicAdd(&s_block[slot % kSlotRing], 0u);
         blk = __shfl_sync(0xffffffffu, blk, 0);
         if (blk >= total) break;
-        const unsigned view = blk / per_view;
-        unsigned rem = blk - view * per_view;
+        const unsigned view = blk / local_per_view;
+        unsigned rem = (blk - view * local_per_view) * sc + si;   // hand-out position in the view
         if (order != nullptr) rem = __ldg(order + rem);   // block hand-out order (see launch_render)
         unsigned long long t_tile = 0;
         if (timeline != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_tile));

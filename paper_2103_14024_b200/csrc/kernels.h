@@ -11,6 +11,9 @@ namespace po {
 struct RenderOpts {
     float gamma;
     float bg[3];
+    // tile sharding of the render (po_render_shard): this launch takes the blocks of hand-out
+    // position k with k % shard_count == shard_index
+    int32_t shard_index = 0, shard_count = 1;
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.

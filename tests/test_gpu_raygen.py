@@ -50,3 +50,24 @@ def test_render_equals_render_rays_of_camera_rays(env, c1_tree):
     rays = po.po_camera_rays(ct, 800, 800).reshape(-1, 6)
     img2 = po.po_render_rays(tree, rays).reshape(img.shape)
     assert torch.equal(img, img2)
+
+
+def test_tile_shards_assemble_the_frame():
+    """po_render_shard: the shards' blocks are disjoint, cover the image, and their sum is
+    bit-identical to po_render (SURVEY 8(e) single-view latency mode)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import gen
+    import paper_2103_14024_b200 as po
+    tree = po.tree_from_gen(gen.scene_random(77, depth=5, sh_degree=2, sigma_scale=3.0))
+    cams = po.cams_tensor(np.concatenate([gen.orbit_camera(3.0, 10.0 + 50 * i, 20.0, 100, 72, 80.0)
+                                          for i in range(2)]))
+    full = po.po_render(tree, cams, 100, 72)
+    for n in (1, 3, 4):
+        parts = [po.po_render_shard(tree, cams, 100, 72, i, n) for i in range(n)]
+        written = [(p != 0).any(dim=-1) for p in parts]
+        assert int(sum(w.int() for w in written).max()) <= 1          # disjoint
+        assert torch.equal(sum(parts), full)                           # exact assembly
+    with pytest.raises(po.PoError):
+        po.po_render_shard(tree, cams, 100, 72, 3, 3)
