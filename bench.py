@@ -405,7 +405,7 @@ def run_c4(args):
     torch.cuda.synchronize()
     gt.destroy()
     opt = OctreeOptimizer(tree, lr=args.lr, gamma=0.0, device=dev, chunks=args.chunks, max_seg=args.max_seg,
-                          deterministic=args.deterministic)
+                          deterministic=args.deterministic, reduce_scatter=args.reduce_scatter)
     # algorithmic bytes of the dominant kernel (k_backward, pass 2 with aux) over the timed batches
     visits = nodes = 0
     for rays, _ in batches[args.warmup:]:
@@ -479,6 +479,9 @@ def run_c4(args):
                                                            else " (unsorted)"),
                        "ray_order": args.ray_order, "pass2_chunks": opt.n_chunks(),
                        "pass2_reduction": "deterministic segmented" if args.deterministic else "atomic",
+                       "gradient_sync": ("reduce-scatter + shard SGD + all-gather" if opt.reduce_scatter else
+                                         ("allreduce overlapped with pass-2 chunks" if opt.n_chunks() > 1 else
+                                          ("bucketed allreduce" if ws > 1 else "none (1 GPU)"))),
                        "pass2": (f"stored segments (max {args.max_seg}/ray, {args.max_seg * n_rays * 32 / 2**30:.1f} GiB)"
                                  if args.max_seg > 0 else "re-traversal")},
             "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
@@ -572,6 +575,8 @@ def main():
                     help="analysis only: 'orbit' = consecutive orbit views without flushing (warm, realistic "
                          "frame-to-frame reuse), 'same' = one view repeated; the reported number uses 'flush'")
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
+    ap.add_argument("--reduce-scatter", action="store_true",
+                    help="c4 at N>1: SGD fused into the gradient collective (reduce-scatter, shard update, all-gather)")
     ap.add_argument("--deterministic", action="store_true",
                     help="c4: order-fixed pass 2 (segmented reduction instead of atomics)")
     ap.add_argument("--max-seg", type=int, default=256,

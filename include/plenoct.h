@@ -99,6 +99,14 @@ po_status po_tree_set_sg_basis(po_tree* tree, const float* axes, const float* la
  * po_tree_read_leaves this snapshots / restores a tree during optimisation (early stopping). */
 po_status po_tree_write_leaves(po_tree* tree, const float* sigma, const float* sh);
 
+/* Device pointers to the tree's own leaf payload, for collectives that update it in place
+ * (reduce-scatter SGD: each rank updates its leaf shard, then an all-gather writes every
+ * shard into every rank's tree).  sigma: float[capacity]; sh: rows of sh_row elements (fp32 or
+ * fp16 per the payload), [capacity][sh_row]; capacity = n_leaves + 4096 spare zeroed leaves
+ * that no node references, so equal-size chunks may run past n_leaves.  The tree keeps
+ * ownership; writes must be stream-ordered after the renders that read the tree. */
+po_status po_tree_leaf_payload(po_tree* tree, float** sigma, void** sh, int32_t* sh_row, int64_t* capacity);
+
 /* Export (NEXT f2; "the entire optimization process is done in float32 ... after it we
  * store the PlenOctree with float16"): a new tree with the same structure and leaf values
  * re-uploaded with `payload` (PO_F16: SH coefficients rounded to nearest-even, sigma~ stays

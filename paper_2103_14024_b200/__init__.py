@@ -24,7 +24,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
           5: "PO_ERR_UNSUPPORTED"}
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
-           "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis",
+           "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis", "po_tree_leaf_payload",
            "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
@@ -90,6 +90,7 @@ def lib():
         L.po_tree_convert.argtypes = [P, I32, ctypes.POINTER(P)]
         L.po_tree_write_leaves.argtypes = [P, P, P]
         L.po_tree_set_sg_basis.argtypes = [P, P, P]
+        L.po_tree_leaf_payload.argtypes = [P, P, P, P, P]
         L.po_tree_info.argtypes = [P, P, P, P]
         L.po_tree_read_leaves.argtypes = [P, P, P]
         L.po_render.argtypes = [P, P, I32, I32, I32, P, P, P]
@@ -125,6 +126,8 @@ def _ptr(x):
     """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
     if x is None:
         return None
+    if isinstance(x, int):   # a raw device address (e.g. an offset view for a shard)
+        return x
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     return x.data_ptr()
@@ -199,6 +202,27 @@ class PlenOctree:
         axes = np.ascontiguousarray(axes, dtype=np.float32).reshape(self.B, 3)
         lam = np.ascontiguousarray(lam, dtype=np.float32).reshape(self.B)
         _check(lib().po_tree_set_sg_basis(self.handle, _ptr(axes), _ptr(lam)))
+
+    def payload_views(self):
+        """(sigma [capacity], sh rows [capacity][sh_row]) as torch views of the tree's own fp32
+        device arrays (po_tree_leaf_payload); capacity includes the zeroed spare leaves."""
+        import torch
+        if self.desc.payload != PO_F32:
+            raise ValueError("payload views are for fp32 trees")
+        sig, sh = ctypes.c_void_p(), ctypes.c_void_p()
+        row, cap = ctypes.c_int32(), ctypes.c_int64()
+        _check(lib().po_tree_leaf_payload(self.handle, ctypes.byref(sig), ctypes.byref(sh), ctypes.byref(row),
+                                          ctypes.byref(cap)))
+
+        class _Dev:   # __cuda_array_interface__ wrapper (torch.as_tensor makes a zero-copy view)
+            def __init__(self, ptr, shape):
+                self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f4", "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+
+        dev = torch.device("cuda", self.device)
+        s_t = torch.as_tensor(_Dev(sig.value, (cap.value,)), device=dev)
+        k_t = torch.as_tensor(_Dev(sh.value, (cap.value, row.value)), device=dev)
+        return s_t, k_t
 
     def destroy(self):
         if self._h is not None:

@@ -44,6 +44,7 @@ struct po_tree {
     int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
     unsigned* work_of(int slot) { return d_work + 2 * slot; }
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
+    static constexpr int64_t kPayloadPad = 4096;   // spare zero leaves after the payload arrays
     float4* d_sg = nullptr;          // spherical-Gaussian lobes (po_tree_set_sg_basis) or null
     std::vector<float> h_sg;         // the same on the host, [B][4]
     // po_render_backward_deterministic scratch, grown on demand
@@ -258,9 +259,16 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     };
     cudaError_t e = cudaMalloc(&t->d_child, (size_t)n_nodes * 8 * sizeof(uint32_t));
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(child)"));
-    e = cudaMalloc(&t->d_sigma, (size_t)std::max<int64_t>(n_leaves, 1) * sizeof(float));
+    // payload arrays carry kPayloadPad zeroed spare leaves at the end (never referenced by the
+    // child table) so sharded updates can gather equal-size leaf chunks in place
+    // (po_tree_leaf_payload, reduce-scatter SGD)
+    const int64_t n_alloc = n_leaves + po_tree::kPayloadPad;
+    e = cudaMalloc(&t->d_sigma, (size_t)n_alloc * sizeof(float));
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sigma)"));
-    e = cudaMalloc(&t->d_sh, (size_t)std::max<int64_t>(n_leaves, 1) * row * elt);
+    e = cudaMalloc(&t->d_sh, (size_t)n_alloc * row * elt);
+    if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
+    if ((e = cudaMemset(t->d_sigma, 0, (size_t)n_alloc * sizeof(float))) == cudaSuccess)
+        e = cudaMemset(t->d_sh, 0, (size_t)n_alloc * row * elt);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
     e = cudaMalloc(&t->d_work, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
@@ -357,6 +365,15 @@ po_status po_tree_write_leaves(po_tree* t, const float* sigma, const float* sh) 
         }
     if ((e = cudaMemcpy(t->d_sh, buf.data(), buf.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
         return cuda_status(e, "write sh");
+    return PO_OK;
+}
+
+po_status po_tree_leaf_payload(po_tree* t, float** sigma, void** sh, int32_t* sh_row, int64_t* capacity) {
+    if (po_status s = check_tree(t)) return s;
+    if (sigma) *sigma = t->d_sigma;
+    if (sh) *sh = t->d_sh;
+    if (sh_row) *sh_row = t->sh_row;
+    if (capacity) *capacity = t->n_leaves + po_tree::kPayloadPad;
     return PO_OK;
 }
 

@@ -117,3 +117,32 @@ def agree_bounds(bounds, n_leaves: int, group=None, world_size: int = 1):
     for j in range(1, len(out)):
         out[j] = max(out[j], out[j - 1])
     return out
+
+
+def shard_chunk(n_leaves: int, world_size: int, align: int = 4) -> int:
+    """Leaves per rank for the reduce-scatter SGD: equal chunks, a multiple of `align` (keeps
+    every shard's SH gradient rows 16-B aligned), covering n_leaves; chunk * world_size may run
+    past n_leaves into the tree's zeroed spare leaves (po_tree_leaf_payload)."""
+    c = -(-max(1, n_leaves) // max(1, world_size))
+    return -(-c // align) * align
+
+
+def reduce_scatter_sgd(flat_sigma, flat_sh, ne: int, n_leaves: int, chunk: int, rank: int, world_size: int, sgd_shard,
+                       payload_sigma, payload_sh, group=None):
+    """SGD fused into the gradient collective (NEXT f2): reduce-scatter gives rank r the summed
+    gradient of leaves [r c, (r+1) c) only, the rank updates that shard (sgd_shard(gs, gk, b, e)
+    with e clipped to n_leaves) -- 1/N of the update work -- and an in-place all-gather writes
+    every rank's updated shard into every tree.  Same bytes on the wire as allreduce + SGD."""
+    import torch
+    import torch.distributed as dist
+    dev = flat_sigma.device
+    gs = torch.empty(chunk, dtype=flat_sigma.dtype, device=dev)
+    gk = torch.empty(chunk * ne, dtype=flat_sh.dtype, device=dev)
+    dist.reduce_scatter_tensor(gs, flat_sigma[:chunk * world_size], group=group)
+    dist.reduce_scatter_tensor(gk, flat_sh[:chunk * world_size * ne], group=group)
+    b = rank * chunk
+    e = min(n_leaves, b + chunk)
+    if e > b:
+        sgd_shard(gs, gk, b, e)
+    dist.all_gather_into_tensor(payload_sigma[:chunk * world_size], payload_sigma[b:b + chunk], group=group)
+    dist.all_gather_into_tensor(payload_sh[:chunk * world_size], payload_sh[b:b + chunk], group=group)

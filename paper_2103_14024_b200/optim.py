@@ -25,13 +25,14 @@ import torch
 from . import (Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk,
                po_render_backward_deterministic, po_render_rays,
                po_tree_sgd_step_range)
-from .dist import agree_bounds, allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets
+from .dist import (agree_bounds, allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets,
+                   reduce_scatter_sgd, shard_chunk)
 
 
 class OctreeOptimizer:
     def __init__(self, tree, lr: float, gamma: float = 0.0, background=(1.0, 1.0, 1.0), group=None,
                  bucket_mb: float = 64.0, device=None, chunks=None, max_seg: int = 256,
-                 deterministic: bool = False):
+                 deterministic: bool = False, reduce_scatter: bool = False):
         self.tree = tree
         self.lr = float(lr)
         self.gamma = float(gamma)
@@ -39,10 +40,18 @@ class OctreeOptimizer:
         self.group = group
         self.device = torch.device("cuda", tree.device) if device is None else torch.device(device)
         n, B = tree.n_leaves, tree.B
-        _, self.sh_off, total = flat_layout(n, B)
+        # reduce-scatter SGD (NEXT f2): equal leaf chunks per rank; the flat gradient is padded
+        # to chunk * world_size leaves in both regions so the collectives split it evenly
+        self.reduce_scatter = bool(reduce_scatter) and self.world_size > 1
+        self.chunk = shard_chunk(n, self.world_size) if self.reduce_scatter else 0
+        if self.reduce_scatter:
+            self.sh_off = self.chunk * self.world_size
+            total = self.sh_off + self.sh_off * 3 * B
+        else:
+            _, self.sh_off, total = flat_layout(n, B)
         self.flat = torch.zeros(total, dtype=torch.float32, device=self.device)
         self.grad_sigma = self.flat[:n]
-        self.grad_sh = self.flat[self.sh_off:].view(n, B, 3)
+        self.grad_sh = self.flat[self.sh_off:self.sh_off + n * 3 * B].view(n, B, 3)
         self.buckets = plan_buckets(total, int(bucket_mb * (1 << 20)) // 4)
         self._bufs = {}
         self.loss = torch.zeros(1, dtype=torch.float64, device=self.device)
@@ -88,6 +97,8 @@ class OctreeOptimizer:
         # the gradient buffer is zero here: it starts zeroed and every SGD call below zeroes
         # what it consumed (PO_SGD_ZERO_GRAD), which replaces a 0.7 GB memset per step
         nl = self.tree.n_leaves
+        if self.reduce_scatter:
+            K = 1
         if K > 1 and self.deterministic:
             raise ValueError("deterministic pass 2 is not combined with the chunked overlap")
         if K > 1:
@@ -136,6 +147,20 @@ class OctreeOptimizer:
         else:
             po_render_backward(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux=aux, gamma=self.gamma,
                                background=self.background, segments=seg)
+        if self.reduce_scatter:
+            ne = 3 * self.tree.B
+            sig_view, sh_view = self.tree.payload_views()
+
+            def sgd_shard(gs, gk, b, e):   # gradient index b sits at gs[0] / gk[0]
+                po_tree_sgd_step_range(self.tree, gs.data_ptr() - 4 * b, gk.data_ptr() - 4 * b * ne, self.lr, b, e)
+                po_tree_sgd_step_range(self.tree, gs.data_ptr() - 4 * b, gk.data_ptr() - 4 * b * ne, self.lr,
+                                       nl + b * ne, nl + e * ne)
+
+            reduce_scatter_sgd(self.flat[:self.sh_off], self.flat[self.sh_off:], ne, nl, self.chunk,
+                               torch.distributed.get_rank(self.group), self.world_size, sgd_shard, sig_view, sh_view,
+                               self.group)
+            self.flat.zero_()   # the shard buffers were consumed; the flat gradient starts at 0 again
+            return self.loss
         if self.world_size > 1:
             works = allreduce_buckets(self.flat, self.buckets, self.group)
             for (s, e), w in zip(self.buckets, works):
