@@ -497,6 +497,49 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float*
     }
 }
 
+// Measurement variants of the plain forward over a ray list (PO_RAYS_OPT, SH-3 fp32 only):
+// 128 = the default lean step, 64 = traversal + T only (wrong colours).  Used by
+// tools/diag_tail.py to time single warp tiles alone ("where the tail comes from").
+template <int OPT>
+__global__ void __launch_bounds__(256, 2) k_render_rays_diag(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                          RenderOpts opt, float* __restrict__ out) {
+    PO_DECLARE_STACK(stk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __ldg(rays + i * 6 + k);
+        d[k] = __ldg(rays + i * 6 + 3 + k);
+    }
+    RayState r;
+    float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
+    if (ray_setup(tr, o, d, r)) {
+        if constexpr (OPT == kOptProbeNoShade) {
+            struct Probe {
+                const DevTree& tr;
+                float T, gamma;
+                __device__ __forceinline__ void on_node() {}
+                __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+                    const float st = __ldg(tr.sigma + idx);
+                    if (!(st > 0.f)) return true;
+                    T = absorb(T, st, __fsub_rn(t1, t0)).Tn;
+                    return !(T < gamma);
+                }
+            } v{tr, 1.f, opt.gamma};
+            traverse<kOptLean>(tr, r, v, stk);
+            C[0] = C[1] = C[2] = v.T;
+        } else {
+            FwdVisitor<3, false> v(tr, r.d, opt.gamma);
+            traverse<OPT>(tr, r, v, stk);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
+        }
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) out[i * 3 + ch] = C[ch];
+}
+
 struct SegIn {
     const float4* __restrict__ rec;
     const int32_t* __restrict__ count;
@@ -1137,6 +1180,17 @@ cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float
                                cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const SegOut so{static_cast<float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+    static const int dopt = [] {   // measurement variants (k_render_rays_diag)
+        const char* e = getenv("PO_RAYS_OPT");
+        return e ? atoi(e) : 0;
+    }();
+    if (dopt != 0 && deg == 3 && !f16 && aux == nullptr) {
+        if (dopt == kOptProbeNoShade)
+            k_render_rays_diag<kOptProbeNoShade><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out);
+        else
+            k_render_rays_diag<kOptLean><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out);
+        return cudaGetLastError();
+    }
     PO_DISPATCH(deg, f16, {
         carveout_once(k_render_rays<DEG, F16>);
         k_render_rays<DEG, F16><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out, aux, span, so);
