@@ -405,7 +405,8 @@ def run_c4(args):
     torch.cuda.synchronize()
     gt.destroy()
     opt = OctreeOptimizer(tree, lr=args.lr, gamma=0.0, device=dev, chunks=args.chunks, max_seg=args.max_seg,
-                          deterministic=args.deterministic, reduce_scatter=args.reduce_scatter)
+                          deterministic=args.deterministic, reduce_scatter=args.reduce_scatter,
+                          fused_sgd=not args.unfused_sgd)
     # algorithmic bytes of the dominant kernel (k_backward, pass 2 with aux) over the timed batches
     visits = nodes = 0
     for rays, _ in batches[args.warmup:]:
@@ -467,6 +468,7 @@ def run_c4(args):
     if rank == 0:
         peak, peak_src = _peaks()
         alg = (visits * (4 + 192 + 196) + nodes * 32) / K + n_rays * (24 + 12 + 32)
+        fused = (opt.fused_sgd and ws == 1 and not args.deterministic and args.max_seg > 0 and opt.n_chunks() == 1)
         line = {
             "metric": "direct octree optimisation rays/s (c4: forward+backward+allreduce+SGD)",
             "value": round(rays_per_s, 1), "unit": "rays/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
@@ -483,7 +485,10 @@ def run_c4(args):
                                          ("allreduce overlapped with pass-2 chunks" if opt.n_chunks() > 1 else
                                           ("bucketed allreduce" if ws > 1 else "none (1 GPU)"))),
                        "pass2": (f"stored segments (max {args.max_seg}/ray, {args.max_seg * n_rays * 32 / 2**30:.1f} GiB)"
-                                 if args.max_seg > 0 else "re-traversal")},
+                                 if args.max_seg > 0 else "re-traversal"),
+                       "update": ("SGD fused into pass 2 (po_render_backward_sgd: -lr*gradient added straight "
+                                  "into the tree, no gradient buffer)" if fused else
+                                  "gradient buffer + SGD pass (po_tree_sgd_step_range)")},
             "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
             "leaf_visits_per_step": visits / K,
             "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
@@ -577,6 +582,8 @@ def main():
     ap.add_argument("--rays", type=int, default=1 << 20, help="c4: rays per GPU per step")
     ap.add_argument("--reduce-scatter", action="store_true",
                     help="c4 at N>1: SGD fused into the gradient collective (reduce-scatter, shard update, all-gather)")
+    ap.add_argument("--unfused-sgd", action="store_true",
+                    help="c4 at N=1: separate gradient buffer + SGD pass instead of po_render_backward_sgd")
     ap.add_argument("--deterministic", action="store_true",
                     help="c4: order-fixed pass 2 (segmented reduction instead of atomics)")
     ap.add_argument("--max-seg", type=int, default=256,

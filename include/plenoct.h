@@ -239,6 +239,22 @@ po_status po_render_backward_chunk(const po_tree* tree, const float* rays, const
                                    const double* aux, const po_segments* segments, const po_render_opts* opts,
                                    float* grad_sigma, float* grad_sh, po_stream stream);
 
+/* a8 + a9 fused for a single replica (one GPU, no gradient exchange): pass 2 with the plain
+ * SGD update of P:492 / P:973 folded into it.  Each stored segment's contribution, times -lr,
+ * is added atomically straight into the tree's sigma~ and k (so sigma~ -= lr * dL/dsigma~ and
+ * k -= lr * dL/dk over the whole batch, Eq. 3's sum over rays), with no gradient buffer
+ * and no separate update pass.  Equal to po_render_backward + po_tree_sgd_step up to the fp32
+ * summation order.  Needs aux and segments from the po_render_rays call of this batch on this
+ * tree (the tree must not change in between); rays whose segments overflowed max_seg are
+ * re-traversed FIRST (on the unmodified tree) into grad_sigma / grad_sh, which must be zero on
+ * entry and are applied and zeroed again at the end (a no-op launch when no ray overflowed).
+ * fp32 trees only (PO_ERR_UNSUPPORTED otherwise); lr finite.  Mutates the tree: stream-order it
+ * after every render that reads the tree, as for po_tree_sgd_step.  Not for world_size > 1,
+ * where the summed gradient must cross ranks first. */
+po_status po_render_backward_sgd(po_tree* tree, const float* rays, int64_t n, const float* dL_dC, const double* aux,
+                                 const po_segments* segments, const po_render_opts* opts, float lr,
+                                 float* grad_sigma, float* grad_sh, po_stream stream);
+
 /* Deterministic pass 2 (NEXT f2 "deterministic-reduction mode"): the same gradients as
  * po_render_backward with stored segments, accumulated by a segmented reduction instead of
  * atomics -- every segment's contribution is emitted with its leaf as key, the records are

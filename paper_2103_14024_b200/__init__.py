@@ -26,7 +26,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
            "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis", "po_tree_leaf_payload",
            "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
-           "po_render_backward", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
+           "po_render_backward", "po_render_backward_sgd", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
            "po_render_timeline"]
 
@@ -103,6 +103,7 @@ def lib():
         L.po_render_depth.argtypes = [P, P, I64, P, P, P, P]
         L.po_leaf_max_alpha.argtypes = [P, P, I64, P, P, P]
         L.po_render_backward.argtypes = [P, P, I64, P, P, P, P, P, P, P]
+        L.po_render_backward_sgd.argtypes = [P, P, I64, P, P, P, P, F, P, P, P]
         L.po_render_backward_deterministic.argtypes = [P, P, I64, P, P, P, P, P, P, P, P]
         L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
         L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
@@ -398,6 +399,22 @@ def po_render_backward(tree: PlenOctree, rays, dL_dC, grad_sigma, grad_sh, aux=N
     o = _opts(gamma, background)
     _check(lib().po_render_backward(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux), _seg(segments),
                                     ctypes.byref(o), _ptr(grad_sigma), _ptr(grad_sh), _stream(stream)))
+
+
+def po_render_backward_sgd(tree: PlenOctree, rays, dL_dC, lr: float, grad_sigma, grad_sh, aux, segments,
+                           gamma: float = 0.0, background=(1.0, 1.0, 1.0), stream=None):
+    """a8 + a9 fused for one replica: sigma~ -= lr dL/dsigma~, k -= lr dL/dk in place on the tree.
+    grad_sigma / grad_sh are zero scratch for rays that overflowed the stored segments (zero again
+    on return); aux and segments come from this batch's po_render_rays (include/plenoct.h)."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    _need(dL_dC, torch.float32, (3,))
+    _need(grad_sigma, torch.float32)
+    _need(grad_sh, torch.float32, (tree.B, 3))
+    _need(aux, torch.float64, (4,))
+    o = _opts(gamma, background)
+    _check(lib().po_render_backward_sgd(tree.handle, _ptr(rays), rays.shape[0], _ptr(dL_dC), _ptr(aux), _seg(segments),
+                                        ctypes.byref(o), float(lr), _ptr(grad_sigma), _ptr(grad_sh), _stream(stream)))
 
 
 def po_render_depth(tree: PlenOctree, rays, gamma: float = 0.01, alpha=None, depth=None, stream=None):

@@ -270,9 +270,10 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
     if ((e = cudaMemset(t->d_sigma, 0, (size_t)n_alloc * sizeof(float))) == cudaSuccess)
         e = cudaMemset(t->d_sh, 0, (size_t)n_alloc * row * elt);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
-    e = cudaMalloc(&t->d_work, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
+    // work counters + one device flag (po_render_backward_sgd: "an overflow ray wrote the buffer")
+    e = cudaMalloc(&t->d_work, sizeof(unsigned) * (2 * po_tree::kWorkSlots + 1));
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
-    e = cudaMemset(t->d_work, 0, sizeof(unsigned) * 2 * po_tree::kWorkSlots);
+    e = cudaMemset(t->d_work, 0, sizeof(unsigned) * (2 * po_tree::kWorkSlots + 1));
     if (e != cudaSuccess) return cleanup(cuda_status(e, "memset(work)"));
     // the device child table is the caller's (ABI encoding, reading Q1)
     e = cudaMemcpy(t->d_child, child, (size_t)n_nodes * 8 * sizeof(uint32_t), cudaMemcpyHostToDevice);
@@ -734,6 +735,31 @@ po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, con
     return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
                                         sg, o, grad_sigma, grad_sh, (cudaStream_t)stream),
                     "po_render_backward");
+}
+
+po_status po_render_backward_sgd(po_tree* t, const float* rays, int64_t n, const float* dL_dC, const double* aux,
+                                 const po_segments* segments, const po_render_opts* opts, float lr,
+                                 float* grad_sigma, float* grad_sh, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (t->desc.payload != PO_F32) return fail(PO_ERR_UNSUPPORTED, "po_render_backward_sgd needs an fp32 payload");
+    if (!std::isfinite(lr)) return fail(PO_ERR_INVALID_ARG, "lr is not finite");
+    if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
+    if (!segments || !aux) return fail(PO_ERR_INVALID_ARG, "po_render_backward_sgd needs aux and segments");
+    po::Segments sg;
+    if (po_status s = check_segments(segments, n, aux, &sg)) return s;
+    if (n == 0) return PO_OK;
+    if (!rays || !dL_dC || !grad_sigma || !grad_sh) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    g_launches.fetch_add(2);   // overflow re-traversal + fused replay + gated SGD
+    return launched(po::launch_backward_sgd(dev_tree(t), t->desc.sh_degree, rays, n, dL_dC, aux, sg, o, t->d_sigma,
+                                            static_cast<float*>(t->d_sh), t->sh_row, t->n_leaves, lr, grad_sigma,
+                                            grad_sh, reinterpret_cast<int*>(t->d_work + 2 * po_tree::kWorkSlots),
+                                            (cudaStream_t)stream),
+                    "po_render_backward_sgd");
 }
 
 static cudaError_t grow(void** p, size_t* cap, size_t need) {

@@ -600,10 +600,13 @@ template <int DEG, bool F16, bool kSkipReplay>
 __global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                   const float* __restrict__ dL_dC, const double* __restrict__ aux,
                                                   SegIn si, RenderOpts opt, float* __restrict__ grad_sigma,
-                                                  float* __restrict__ grad_sh) {
+                                                  float* __restrict__ grad_sh, int* __restrict__ overflow_flag) {
     PO_DECLARE_STACK(stk);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if constexpr (kSkipReplay) {   // po_render_backward_sgd: some ray's gradient went to the buffer
+        if (overflow_flag != nullptr && __ldg(si.count + i) > si.max_seg) *overflow_flag = 1;
+    }
     backward_ray<DEG, F16, kSkipReplay>(tr, rays, i, dL_dC, aux, si, opt, grad_sigma, grad_sh, stk);
 }
 
@@ -721,6 +724,49 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const fl
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= n) return;
     AtomicSink<DEG> sink{grad_sigma, grad_sh};
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
+}
+
+// a8 + a9 fused (po_render_backward_sgd, one replica): each segment's contribution scaled by
+// -lr goes straight into the tree's own sigma~ and padded SH rows, so plain SGD
+// needs no gradient buffer and no separate update pass (the update is linear in the summed
+// gradient; only the fp32 summation order differs from gradient-then-SGD)
+template <int DEG>
+struct SgdSink {
+    float* __restrict__ sigma;
+    float* __restrict__ sh;
+    int32_t sh_row;
+    float neg_lr;
+    __device__ __forceinline__ void operator()(int32_t, uint32_t idx, float gsig, const float gz[3], const float* Y) {
+        constexpr int NE = 3 * ShDim<DEG>::B;
+        atomicAdd(sigma + idx, neg_lr * gsig);
+        float* row = sh + (size_t)idx * sh_row;
+        if constexpr (NE % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < NE / 4; ++j) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = neg_lr * (gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3]);
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * j), "f"(v[0]),
+                             "f"(v[1]), "f"(v[2]), "f"(v[3])
+                             : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int el = 0; el < NE; ++el) atomicAdd(row + el, neg_lr * (gz[el % 3] * Y[el / 3]));
+        }
+    }
+};
+
+template <int DEG>
+__global__ void __launch_bounds__(256, 3) k_backward_replay_sgd(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                             const float* __restrict__ dL_dC,
+                                                             const double* __restrict__ aux, SegIn si,
+                                                             float* __restrict__ sigma, float* __restrict__ sh,
+                                                             int32_t sh_row, float neg_lr) {
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= n) return;
+    SgdSink<DEG> sink{sigma, sh, sh_row, neg_lr};
     replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
 }
 
@@ -1009,7 +1055,8 @@ __global__ void __launch_bounds__(256) k_l2_loss(const float* __restrict__ pred,
 __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ sigma, float* __restrict__ sh, int32_t sh_row,
                                              int32_t ne, int64_t n_leaves, float* __restrict__ grad_sigma,
                                              float* __restrict__ grad_sh, float lr, int64_t begin, int64_t end,
-                                             bool zero_grad) {
+                                             bool zero_grad, const int* __restrict__ gate) {
+    if (gate != nullptr && *gate == 0) return;   // po_render_backward_sgd: the buffer is all zero
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = begin + tid; i < min(end, n_leaves); i += nth) {
@@ -1276,11 +1323,11 @@ cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* r
                 k_backward_replay<DEG><<<grid1d(n, 8), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, grad_sigma, grad_sh);
             carveout_once(k_backward<DEG, F16, true>);
             k_backward<DEG, F16, true><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, opt, grad_sigma,
-                                                                      grad_sh);
+                                                                      grad_sh, nullptr);
         } else {
             carveout_once(k_backward<DEG, F16, false>);
             k_backward<DEG, F16, false><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, opt, grad_sigma,
-                                                                       grad_sh);
+                                                                       grad_sh, nullptr);
         }
     });
     return cudaGetLastError();
@@ -1336,7 +1383,33 @@ cudaError_t launch_sgd(float* sigma, float* sh, int32_t sh_row, int32_t ne, int6
     if (end <= begin) return cudaSuccess;
     unsigned g = grid1d(end - begin, 256 * 4);
     if (g > 148 * 16) g = 148 * 16;
-    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr, begin, end, zero_grad);
+    k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr, begin, end, zero_grad, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward_sgd(const DevTree& tr, int deg, const float* rays, int64_t n, const float* dL_dC,
+                                const double* aux, const Segments& sg, const RenderOpts& opt, float* sigma, float* sh,
+                                int32_t sh_row, int64_t n_leaves, float lr, float* grad_sigma, float* grad_sh,
+                                int* flag, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const SegIn si{static_cast<const float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    PO_DISPATCH(deg, false, {
+        // 1. rays whose segments overflowed: re-traversal of the tree as it is, into the buffer
+        carveout_once(k_backward<DEG, false, true>);
+        k_backward<DEG, false, true><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, opt, grad_sigma,
+                                                                    grad_sh, flag);
+        // 2. stored segments: -lr * gradient straight into the payload
+        carveout_once(k_backward_replay_sgd<DEG>);
+        k_backward_replay_sgd<DEG><<<grid1d(n, 8), 256, 0, s>>>(tr, rays, n, dL_dC, aux, si, sigma, sh, sh_row, -lr);
+        // 3. the buffer's SGD (and zeroing), a no-op launch unless step 1 wrote to it
+        const int ne = 3 * ShDim<DEG>::B;
+        const int64_t end = n_leaves * (1 + ne);
+        unsigned g = grid1d(end, 256 * 4);
+        if (g > 148 * 16) g = 148 * 16;
+        k_sgd<<<g, 256, 0, s>>>(sigma, sh, sh_row, ne, n_leaves, grad_sigma, grad_sh, lr, 0, end, true, flag);
+    });
     return cudaGetLastError();
 }
 

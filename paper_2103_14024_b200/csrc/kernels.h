@@ -60,6 +60,13 @@ cudaError_t launch_plan_ends(const uint32_t* sorted_keys, int64_t n, int64_t n_l
 cudaError_t launch_backward(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n, const float* dL_dC,
                             const double* aux, const Segments& sg, const RenderOpts& opt, float* grad_sigma,
                             float* grad_sh, cudaStream_t s, bool overflow_only = false);
+// a8 + a9 fused for one replica (po_render_backward_sgd): overflow rays into grad_* (zero on
+// entry, zero again on exit), stored segments' -lr * gradient straight into sigma / sh (rows of
+// sh_row elements), then the buffer's SGD gated on the device flag the overflow kernel sets.
+cudaError_t launch_backward_sgd(const DevTree& tr, int deg, const float* rays, int64_t n, const float* dL_dC,
+                                const double* aux, const Segments& sg, const RenderOpts& opt, float* sigma, float* sh,
+                                int32_t sh_row, int64_t n_leaves, float lr, float* grad_sigma, float* grad_sh,
+                                int* flag, cudaStream_t s);
 cudaError_t launch_render_depth(const DevTree& tr, const float* rays, int64_t n, float gamma, float* alpha,
                                 float* depth, cudaStream_t s);
 cudaError_t launch_leaf_max_alpha(const DevTree& tr, const float* rays, int64_t n, float gamma, float* max_alpha,

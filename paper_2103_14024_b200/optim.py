@@ -11,6 +11,10 @@ and owns buffers):
   4. SUM allreduce of the flat gradient in buckets (NCCL, only when world_size > 1)
   5. po_tree_sgd_step_range per bucket as soon as that bucket has landed (P:492, P:973 SGD)
 
+On one replica (world_size 1, stored segments, fp32 tree) steps 3-5 are one call,
+po_render_backward_sgd: -lr * gradient goes straight into the tree (fused_sgd=False keeps the
+separate gradient + SGD passes).
+
 With chunks = K > 1 (K = 4 by default when world_size > 1), steps 3-5 overlap:
 pass 1 also records each ray's leaf span, po_backward_plan orders the rays into K chunks,
 and the gradient range a chunk finalises is allreduced while the next chunks run
@@ -22,8 +26,8 @@ from __future__ import annotations
 
 import torch
 
-from . import (Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk,
-               po_render_backward_deterministic, po_render_rays,
+from . import (PO_F32, Segments, po_backward_plan, po_l2_loss_grad, po_render_backward, po_render_backward_chunk,
+               po_render_backward_deterministic, po_render_backward_sgd, po_render_rays,
                po_tree_sgd_step_range)
 from .dist import (agree_bounds, allreduce_buckets, flat_layout, flat_to_param_range, overlapped_chunks, plan_buckets,
                    reduce_scatter_sgd, shard_chunk)
@@ -32,7 +36,7 @@ from .dist import (agree_bounds, allreduce_buckets, flat_layout, flat_to_param_r
 class OctreeOptimizer:
     def __init__(self, tree, lr: float, gamma: float = 0.0, background=(1.0, 1.0, 1.0), group=None,
                  bucket_mb: float = 64.0, device=None, chunks=None, max_seg: int = 256,
-                 deterministic: bool = False, reduce_scatter: bool = False):
+                 deterministic: bool = False, reduce_scatter: bool = False, fused_sgd: bool = True):
         self.tree = tree
         self.lr = float(lr)
         self.gamma = float(gamma)
@@ -63,6 +67,8 @@ class OctreeOptimizer:
         self.max_seg = int(max_seg)
         # order-fixed pass 2 (po_render_backward_deterministic): bit-reproducible gradients
         self.deterministic = bool(deterministic)
+        # one replica: pass 2 writes -lr * gradient straight into the tree (po_render_backward_sgd)
+        self.fused_sgd = bool(fused_sgd)
         if self.deterministic and self.max_seg <= 0:
             raise ValueError("the deterministic backward replays stored segments: max_seg must be > 0")
 
@@ -140,6 +146,11 @@ class OctreeOptimizer:
 
             overlapped_chunks(self.flat, leaf_end, nl, self.tree.B, self.sh_off, run_chunk, apply_final,
                               group=self.group, world_size=self.world_size)
+            return self.loss
+        if (self.fused_sgd and self.world_size == 1 and not self.deterministic and seg is not None
+                and self.tree.desc.payload == PO_F32):
+            po_render_backward_sgd(self.tree, rays, dL, self.lr, self.grad_sigma, self.grad_sh, aux, seg,
+                                   gamma=self.gamma, background=self.background)
             return self.loss
         if self.deterministic:
             po_render_backward_deterministic(self.tree, rays, dL, self.grad_sigma, self.grad_sh, aux, seg,

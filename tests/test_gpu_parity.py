@@ -495,10 +495,13 @@ def test_sgd_range_sparse_and_zeroing(env, deg):
     np.testing.assert_array_equal(flat, flat_ref.astype(np.float32))
 
 
-@pytest.mark.parametrize("chunks,max_seg", [(1, 0), (5, 0), (1, 16), (5, 16)])
-def test_optimizer_step_matches_oracle(env, chunks, max_seg):
+@pytest.mark.parametrize("chunks,max_seg,fused", [(1, 0, True), (5, 0, True), (1, 16, True), (1, 16, False),
+                                                  (5, 16, True), (1, 256, True)])
+def test_optimizer_step_matches_oracle(env, chunks, max_seg, fused):
     """a7..a9 chain (OctreeOptimizer.step, world size 1) vs the oracle's Eq. (3) gradient + SGD;
-    chunks = 5 runs pass 2 + SGD through po_backward_plan's chunks (the overlapped path)."""
+    chunks = 5 runs pass 2 + SGD through po_backward_plan's chunks (the overlapped path).  With
+    stored segments and one chunk the step is po_render_backward_sgd (fused=True): max_seg 16
+    sends many rays through the overflow re-traversal + gated SGD, max_seg 256 none."""
     po, om, torch = env
     from paper_2103_14024_b200.optim import OctreeOptimizer
     t = gen.scene_random(60, depth=5, sh_degree=3, sigma_scale=3.0)
@@ -510,7 +513,7 @@ def test_optimizer_step_matches_oracle(env, chunks, max_seg):
     target = rng(62).random((rays.shape[0], 3)).astype(np.float32)
     tree = po.tree_from_gen(t)
     lr = 1.0   # large enough that fp32 rounding of the updated leaves does not mask the gradient
-    opt = OctreeOptimizer(tree, lr=lr, gamma=0.0, chunks=chunks, max_seg=max_seg)
+    opt = OctreeOptimizer(tree, lr=lr, gamma=0.0, chunks=chunks, max_seg=max_seg, fused_sgd=fused)
     loss = opt.step(_dev(torch, rays), _dev(torch, target)).item()
     ref = om.render(ot, r64, gamma=0.0)
     diff = ref["rgb"] - target.astype(np.float64)
