@@ -325,6 +325,16 @@ po_status po_trace(const po_tree* tree, const float* rays, int64_t n, const po_r
 po_status po_render_stats(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                           const po_render_opts* opts, unsigned long long* counters, po_stream stream);
 
+/* po_ray_step_timing (measurement, SH-3 fp32 trees): the po_render_rays forward of n rays, one
+ * thread each, recording for every box step k < max_steps of ray i two uint32 at
+ * rec[(i * max_steps + k) * 2]: the SM cycles since the previous box step (the previous box's
+ * leaf work, the neighbour step and this box's descent) and (child-entry loads of this descent)
+ * << 8 | (log2 box edge in leaf cells) << 1 | (previous box was a composited leaf).  steps[i] =
+ * number of box steps (may exceed max_steps).  Used to find the critical path of slow warps
+ * (DESIGN.md §6.1); no image is written. */
+po_status po_ray_step_timing(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
+                             int32_t max_steps, uint32_t* rec, int32_t* steps, po_stream stream);
+
 /* po_render_timeline: po_render that also records, for every 8x4-pixel warp tile, device
  * uint64 timeline[ceil(W/16)*ceil(H/16)*n_cams*8][4] = {globaltimer ns at tile start, at tile
  * end, SM id << 32 | block index in its view, view} (scheduling analysis; same image). */

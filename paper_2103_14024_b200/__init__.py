@@ -28,7 +28,7 @@ EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "
            "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_render_backward_sgd", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
-           "po_render_timeline"]
+           "po_render_timeline", "po_ray_step_timing"]
 
 
 class PoError(RuntimeError):
@@ -111,6 +111,7 @@ def lib():
         L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, P]
         L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_timeline.argtypes = [P, P, I32, I32, I32, P, P, P, P]
+        L.po_ray_step_timing.argtypes = [P, P, I64, P, I32, P, P, P]
         for name in EXPORTS:
             if name not in ("po_last_error", "po_version", "po_launch_count"):
                 getattr(L, name).restype = ctypes.c_int
@@ -531,6 +532,19 @@ def po_render_timeline(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.
     _check(lib().po_render_timeline(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), _ptr(out), _ptr(tl),
                                     _stream(stream)))
     return out, tl
+
+
+def po_ray_step_timing(tree: PlenOctree, rays, max_steps: int = 1024, gamma: float = 0.01, stream=None):
+    """Measurement: (rec uint32 [n][max_steps][2], steps int32 [n]) -- include/plenoct.h."""
+    import torch
+    rays = _need(rays, torch.float32, (6,))
+    n = rays.shape[0]
+    rec = torch.zeros((n, max_steps, 2), dtype=torch.int32, device=rays.device)
+    steps = torch.zeros(n, dtype=torch.int32, device=rays.device)
+    o = _opts(gamma, (1.0, 1.0, 1.0))
+    _check(lib().po_ray_step_timing(tree.handle, _ptr(rays), n, ctypes.byref(o), int(max_steps), _ptr(rec),
+                                    _ptr(steps), _stream(stream)))
+    return rec, steps
 
 
 def launch_count() -> int:

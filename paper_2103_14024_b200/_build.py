@@ -30,7 +30,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cu = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"), *cu, "-o", tmp]
+    extra = os.environ.get("PO_NVCC_EXTRA", "").split()   # A/B experiments only (e.g. -DPO_CHILD_LD=1)
+    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"), *cu, "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

@@ -952,6 +952,22 @@ po_status po_render_timeline(const po_tree* t, const po_camera* cams, int32_t n_
                             "po_render_timeline", timeline);
 }
 
+po_status po_ray_step_timing(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts,
+                             int32_t max_steps, uint32_t* rec, int32_t* steps, po_stream stream) {
+    if (po_status s = check_tree(t)) return s;
+    po::RenderOpts o;
+    if (po_status s = check_opts(opts, &o)) return s;
+    if (t->desc.sh_degree != 3 || t->desc.payload != PO_F32)
+        return fail(PO_ERR_UNSUPPORTED, "po_ray_step_timing: SH-3 fp32 trees only");
+    if (n < 0 || max_steps < 0) return fail(PO_ERR_INVALID_ARG, "n or max_steps < 0");
+    if (n == 0) return PO_OK;
+    if (!rays || !rec || !steps) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    return launched(po::launch_ray_step_timing(dev_tree(t), rays, n, o, max_steps, rec, steps, (cudaStream_t)stream),
+                    "po_ray_step_timing");
+}
+
 po_status po_render_stats(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                           const po_render_opts* opts, unsigned long long* counters, po_stream stream) {
     if (po_status s = check_tree(t)) return s;

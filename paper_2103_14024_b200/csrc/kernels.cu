@@ -540,6 +540,69 @@ __global__ void __launch_bounds__(256, 2) k_render_rays_diag(DevTree tr, const f
     for (int ch = 0; ch < 3; ++ch) out[i * 3 + ch] = C[ch];
 }
 
+// Measurement: per-box-step SM cycles of the forward (po_ray_step_timing).  Record k of a ray =
+// (cycles since the previous box step, loads << 8 | shift << 1 | previous box was a shaded leaf):
+// the cycles cover the previous box's leaf work, the neighbour step and this box's descent.
+template <int DEG>
+struct StepTimingVisitor : FwdVisitor<DEG, false> {
+    uint32_t* rec;
+    int32_t max_steps, steps, loads;
+    long long last;
+    bool leaf_prev;
+    __device__ StepTimingVisitor(const DevTree& t, const float d[3], float g) : FwdVisitor<DEG, false>(t, d, g) {}
+    __device__ __forceinline__ void on_node() { ++loads; }
+    __device__ __forceinline__ void on_box(int shift) {
+        const long long now = clock64();
+        if (steps < max_steps) {
+            rec[2 * steps] = (uint32_t)min(now - last, 0xFFFFFFFFll);
+            rec[2 * steps + 1] = ((uint32_t)loads << 8) | ((uint32_t)shift << 1) | (leaf_prev ? 1u : 0u);
+        }
+        ++steps;
+        loads = 0;
+        leaf_prev = false;
+        last = clock64();
+    }
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        leaf_prev = true;
+        return FwdVisitor<DEG, false>::on_leaf(idx, t0, t1);
+    }
+};
+
+__global__ void __launch_bounds__(256, 2) k_ray_step_timing(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                         RenderOpts opt, int32_t max_steps, uint32_t* __restrict__ rec,
+                                                         int32_t* __restrict__ steps) {
+    PO_DECLARE_STACK(stk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[3], d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __ldg(rays + i * 6 + k);
+        d[k] = __ldg(rays + i * 6 + 3 + k);
+    }
+    RayState r;
+    int32_t ns = 0;
+    if (ray_setup(tr, o, d, r)) {
+        StepTimingVisitor<3> v(tr, r.d, opt.gamma);
+        v.rec = rec + (size_t)i * max_steps * 2;
+        v.max_steps = max_steps;
+        v.steps = 0;
+        v.loads = 0;
+        v.leaf_prev = false;
+        v.last = clock64();
+        traverse(tr, r, v, stk);
+        ns = v.steps;
+    }
+    steps[i] = ns;
+}
+
+cudaError_t launch_ray_step_timing(const DevTree& tr, const float* rays, int64_t n, const RenderOpts& opt,
+                                   int32_t max_steps, uint32_t* rec, int32_t* steps, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_ray_step_timing<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tr, rays, n, opt, max_steps, rec, steps);
+    return cudaGetLastError();
+}
+
 struct SegIn {
     const float4* __restrict__ rec;
     const int32_t* __restrict__ count;

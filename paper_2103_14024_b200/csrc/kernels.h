@@ -24,6 +24,8 @@ struct RenderOpts {
 cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera* cams, int n_cams, int W, int H,
                           const RenderOpts& opt, float* out, unsigned* work, const unsigned* order,
                           unsigned long long* timeline, cudaStream_t s);
+cudaError_t launch_ray_step_timing(const DevTree& tr, const float* rays, int64_t n, const RenderOpts& opt,
+                                   int32_t max_steps, uint32_t* rec, int32_t* steps, cudaStream_t s);
 cudaError_t launch_camera_rays(const po_camera* cams, int n_cams, int W, int H, float* rays, cudaStream_t s);
 // stored pass-1 segments (po_segments): rec = float[max_seg][n][8] or null
 struct Segments {
