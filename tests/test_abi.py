@@ -99,6 +99,7 @@ def test_rejects_bad_args_without_gpu(po):
     h = ctypes.c_void_p()
     assert L.po_tree_convert(None, 1, ctypes.byref(h)) == 1 and h.value is None
     assert L.po_tree_sgd_step_range(None, None, None, ctypes.c_float(1.0), 0, 1, 0, None) == 1
+    assert L.po_ray_step_timing(None, None, 1, ctypes.byref(o), 8, None, None, None) == 1
     assert L.po_render_backward_sgd(None, None, 1, None, None, None, ctypes.byref(o), ctypes.c_float(1.0), None, None,
                                     None) == 1
 
