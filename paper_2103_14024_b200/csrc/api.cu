@@ -35,6 +35,9 @@ struct po_tree {
     // centre-out order of the 16x16 pixel blocks of a W x H view (built once per size)
     unsigned* d_order = nullptr;
     int order_w = 0, order_h = 0;
+    // the same, zipped with its reverse (po_render_host writing a pinned image over PCIe)
+    unsigned* d_order_zip = nullptr;
+    int zip_w = 0, zip_h = 0;
     std::mutex order_mu;
     // work counters of the persistent render kernel: kWorkSlots pairs, handed out round
     // robin so up to kWorkSlots renders of one tree may be in flight on different streams
@@ -97,7 +100,7 @@ struct DeviceGuard {
 // centre from the image centre, so the costly on-object blocks of object-centred views go
 // first and the last claims (the tail of the launch) are cheap background blocks.
 // PO_RENDER_ORDER=raster disables it.  Returns NULL for raster order.
-const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_t* err) {
+const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_t* err, bool zip = false) {
     static const bool raster = [] {
         const char* e = getenv("PO_RENDER_ORDER");
         return e && std::strcmp(e, "raster") == 0;
@@ -105,7 +108,10 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
     *err = cudaSuccess;
     if (raster) return nullptr;
     std::lock_guard<std::mutex> lk(t->order_mu);
-    if (t->d_order && t->order_w == W && t->order_h == H) return t->d_order;
+    unsigned*& d_ord = zip ? t->d_order_zip : t->d_order;
+    int& ow = zip ? t->zip_w : t->order_w;
+    int& oh = zip ? t->zip_h : t->order_h;
+    if (d_ord && ow == W && oh == H) return d_ord;
     const int bx = (W + 15) / 16, by = (H + 15) / 16;
     std::vector<unsigned> ord((size_t)bx * by);
     for (size_t i = 0; i < ord.size(); ++i) ord[i] = (unsigned)i;
@@ -115,16 +121,24 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
         return x * x + y * y;
     };
     std::stable_sort(ord.begin(), ord.end(), [&](unsigned a, unsigned b) { return dist(a) < dist(b); });
+    if (zip) {   // centre, border, next-to-centre, next-to-border, ...: image stores spread in time
+        std::vector<unsigned> z;
+        z.reserve(ord.size());
+        for (size_t i = 0, j = ord.size(); i < j;) {
+            z.push_back(ord[i++]);
+            if (i < j) z.push_back(ord[--j]);
+        }
+        ord.swap(z);
+    }
     if ((*err = cudaStreamSynchronize(s)) != cudaSuccess) return nullptr;   // old table may be in use
-    if (t->d_order) cudaFree(t->d_order);
-    t->d_order = nullptr;
-    if ((*err = cudaMalloc(&t->d_order, ord.size() * sizeof(unsigned))) != cudaSuccess) return nullptr;
-    if ((*err = cudaMemcpy(t->d_order, ord.data(), ord.size() * sizeof(unsigned), cudaMemcpyHostToDevice)) !=
-        cudaSuccess)
+    if (d_ord) cudaFree(d_ord);
+    d_ord = nullptr;
+    if ((*err = cudaMalloc(&d_ord, ord.size() * sizeof(unsigned))) != cudaSuccess) return nullptr;
+    if ((*err = cudaMemcpy(d_ord, ord.data(), ord.size() * sizeof(unsigned), cudaMemcpyHostToDevice)) != cudaSuccess)
         return nullptr;
-    t->order_w = W;
-    t->order_h = H;
-    return t->d_order;
+    ow = W;
+    oh = H;
+    return d_ord;
 }
 
 po::DevTree dev_tree(const po_tree* t) {
@@ -412,6 +426,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_work) cudaFree(t->d_work);
     if (t->d_img) cudaFree(t->d_img);
     if (t->d_order) cudaFree(t->d_order);
+    if (t->d_order_zip) cudaFree(t->d_order_zip);
     if (t->d_plan) cudaFree(t->d_plan);
     if (t->d_det) cudaFree(t->d_det);
     if (t->d_sg) cudaFree(t->d_sg);
@@ -477,9 +492,9 @@ static po_status check_cams_host(const po_camera* c, int32_t n) {
 // (An order by measured or probed block cost was tried in r01 and was slower: DESIGN.md §6.1.)
 static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams, int W, int H,
                                   const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
-                                  unsigned long long* timeline = nullptr) {
+                                  unsigned long long* timeline = nullptr, bool zip = false) {
     cudaError_t e = cudaSuccess;
-    const unsigned* order = block_order(t, W, H, s, &e);
+    const unsigned* order = block_order(t, W, H, s, &e, zip);
     if (e != cudaSuccess) return cuda_status(e, "block order");
     const int slot = t->next_slot();
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
@@ -561,7 +576,23 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
             (void)cudaGetLastError();   // pageable memory: not an error
     }
     if (direct) {
-        po_status st = render_scheduled(t, t->d_cams, n_cams, W, H, o, direct, s, "po_render_host");
+        // Block order for in-kernel image stores over PCIe (GPU stores into mapped pinned memory
+        // reach 47-50 GB/s, tools/micro/hostwrite.cu).  Centre-out hands the cheap border blocks
+        // out last, so half the image is stored in a burst near the end of the render and the
+        // PCIe backlog outlasts the kernel; zipping the order with its reverse spreads the stores
+        // over the render.  That pays while the image moves faster than it renders (c1 800x800,
+        // 7.7 MB: 3708 vs 3495 FPS end to end); when the transfer itself is the bound (c3
+        // 1920x1080, 24.9 MB: 1268-1313 vs 1383-1419) centre-out measured better.  Threshold
+        // 12 MiB per launch (~250 us at 50 GB/s, about one c1 render); PO_HOST_ORDER=centre|zip
+        // overrides it.
+        static const int host_order = [] {
+            const char* ev = getenv("PO_HOST_ORDER");
+            if (ev && std::strcmp(ev, "centre") == 0) return 0;
+            if (ev && std::strcmp(ev, "zip") == 0) return 1;
+            return -1;
+        }();
+        const bool zip = host_order >= 0 ? host_order == 1 : out_bytes <= ((size_t)12 << 20);
+        po_status st = render_scheduled(t, t->d_cams, n_cams, W, H, o, direct, s, "po_render_host", nullptr, zip);
         e = cudaStreamSynchronize(s);
         if (st == PO_OK && e != cudaSuccess) st = cuda_status(e, "sync");
         return st;
