@@ -556,8 +556,14 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
         if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(cams)");
         t->cam_cap = n_cams;
     }
-    cudaError_t e = cudaMemcpyAsync(t->d_cams, cams_host, sizeof(po_camera) * (size_t)n_cams, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_status(e, "H2D cams");
+    cudaError_t e = cudaSuccess;
+    if (n_cams == 1) {   // one view travels in the kernel's parameters: no H2D copy on the stream
+        o.cam_inline = 1;
+        std::memcpy(o.cam, cams_host, sizeof(po_camera));
+    } else {
+        e = cudaMemcpyAsync(t->d_cams, cams_host, sizeof(po_camera) * (size_t)n_cams, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_status(e, "H2D cams");
+    }
     const size_t out_bytes = (size_t)n_cams * W * H * 3 * sizeof(float);
     // A pinned (page-locked, device-mapped) output buffer is written by the kernel itself over
     // PCIe while it renders, so the image transfer overlaps the render instead of following

@@ -239,12 +239,7 @@ struct StatsVisitor {
 // ---------------------------------------------------------------------------------------
 // a1: pixel -> ray (reading Q5)
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ void camera_ray(const po_camera* __restrict__ cams, int view, int px, int py, float o[3],
-                                           float d[3]) {
-    const float* cm = reinterpret_cast<const float*>(cams + view);
-    float c[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) c[k] = __ldg(cm + k);
+__device__ __forceinline__ void camera_ray_of(const float c[16], int px, int py, float o[3], float d[3]) {
     // explicit round-to-nearest ops (no FMA contraction): the ray is reproducible bit for bit
     // by any IEEE fp32 implementation of the same expression (po_camera_rays exports it)
     const float dx = __fdiv_rn(__fsub_rn(__fadd_rn((float)px, 0.5f), c[14]), c[12]);
@@ -254,6 +249,15 @@ __device__ __forceinline__ void camera_ray(const po_camera* __restrict__ cams, i
         d[k] = __fsub_rn(__fadd_rn(__fmul_rn(c[k * 4 + 0], dx), __fmul_rn(c[k * 4 + 1], dy)), c[k * 4 + 2]);
         o[k] = c[k * 4 + 3];
     }
+}
+
+__device__ __forceinline__ void camera_ray(const po_camera* __restrict__ cams, int view, int px, int py, float o[3],
+                                           float d[3]) {
+    const float* cm = reinterpret_cast<const float*>(cams + view);
+    float c[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = __ldg(cm + k);
+    camera_ray_of(c, px, py, o, d);
 }
 
 __global__ void __launch_bounds__(256) k_camera_rays(const po_camera* __restrict__ cams, int n_cams, int W, int H,
@@ -387,7 +391,14 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
         if (px < W && py < H) {
             float o[3], d[3];
-            camera_ray(cams, (int)view, px, py, o, d);
+            if (opt.cam_inline) {   // single view passed by value (po_render_host): no H2D copy
+                float c[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) c[k] = opt.cam[k];
+                camera_ray_of(c, px, py, o, d);
+            } else {
+                camera_ray(cams, (int)view, px, py, o, d);
+            }
             RayState r;
             if (ray_setup(tr, o, d, r)) {
                 if constexpr ((OPT & kOptProbeNoShade) != 0) {

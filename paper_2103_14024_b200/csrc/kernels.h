@@ -14,6 +14,9 @@ struct RenderOpts {
     // tile sharding of the render (po_render_shard): this launch takes the blocks of hand-out
     // position k with k % shard_count == shard_index
     int32_t shard_index = 0, shard_count = 1;
+    // k_render only: one view's camera by value (cams unused), so a host camera needs no copy
+    int32_t cam_inline = 0;
+    float cam[16] = {};
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.
