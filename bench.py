@@ -448,17 +448,20 @@ def run_c4(args):
     # rays + targets host -> device inside the timed region and reads the loss back (D2H)
     e2e_steps = min(K, 10)
     host = [(b[0].cpu().pin_memory(), b[1].cpu().pin_memory()) for b in batches[args.warmup:args.warmup + e2e_steps]]
+    opt.train_from_host(host[:2])   # untimed: allocates the pipeline's buffers and side stream
+    host_losses = opt.train_from_host(host)   # untimed warm-up of the full-length call
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for hr, ht in host:
-        loss = opt.step(hr.to(dev, non_blocking=True), ht.to(dev, non_blocking=True))
-        float(loss.item())
+    # OctreeOptimizer.train_from_host: each step's H2D copy overlaps the previous step on a side
+    # stream, each step's loss comes back by an async D2H copy into pinned memory
+    host_losses = opt.train_from_host(host)
     f1.record(stream)
     torch.cuda.synchronize()
+    assert np.isfinite(host_losses.numpy()).all()
     e2e_ms = f0.elapsed_time(f1)
     if ws > 1:
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
@@ -497,8 +500,9 @@ def run_c4(args):
                          "alg_bytes_def": "visits*(4 sigma + 192 SH row + 196 gradient RMW) + nodes*32 + rays*68"},
             "gpu_launches": int(launches), "clocks": clk,
             "e2e": {"value": round(e2e_value, 1), "unit": "rays/s", "h2d_bytes_per_step": n_rays * (24 + 12),
-                    "d2h_bytes_per_step": 8, "entry": "OctreeOptimizer.step on pinned host batches (H2D rays + "
-                                                      "targets, loss read back every step)"},
+                    "d2h_bytes_per_step": 8, "entry": "OctreeOptimizer.train_from_host on pinned host batches (every step's "
+                                                      "rays + targets copied H2D on a side stream overlapping the "
+                                                      "previous step; every step's loss copied D2H, async)"},
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -92,6 +92,56 @@ class OctreeOptimizer:
             return max(1, int(self.chunks))
         return 4 if self.world_size > 1 else 1
 
+    def train_from_host(self, host_batches) -> torch.Tensor:
+        """Steps over (rays [n][6], target [n][3]) batches in PINNED host memory, one step each.
+
+        Batch i+1's host->device copy runs on a side stream while step i computes (two device
+        buffers, each refilled only after the step that read it), and every step's loss is
+        copied device->host into a pinned tensor without blocking.  Returns that pinned float64
+        [len(host_batches)] tensor (reused by the next call with as many batches); it is valid
+        once the current stream has completed (e.g. after torch.cuda.synchronize()).  Every step's inputs still cross PCIe and every loss
+        comes back: the copies overlap compute instead of preceding it."""
+        k = len(host_batches)
+        if k == 0:
+            return torch.empty(0, dtype=torch.float64)
+        n = host_batches[0][0].shape[0]
+        # pipeline resources are allocated once per batch size (pinned and device allocations
+        # synchronise the device, so they stay out of the steady state)
+        key = ("pipe", n)
+        if key not in self._bufs:
+            self._bufs[key] = (torch.cuda.Stream(self.device),
+                               [(torch.empty((n, 6), dtype=torch.float32, device=self.device),
+                                 torch.empty((n, 3), dtype=torch.float32, device=self.device)) for _ in range(2)],
+                               [torch.cuda.Event() for _ in range(2)])
+        copy, bufs, ready = self._bufs[key]
+        if ("losses", k) not in self._bufs:
+            self._bufs[("losses", k)] = torch.empty(k, dtype=torch.float64, pin_memory=True)
+        losses = self._bufs[("losses", k)]
+        main = torch.cuda.current_stream(self.device)
+        copy.wait_stream(main)   # the copies start after everything already queued on main
+        free = [None, None]
+
+        def prefetch(i):
+            b = i % 2
+            with torch.cuda.stream(copy):
+                if free[b] is not None:
+                    copy.wait_event(free[b])   # step i-2 has finished reading buffer b
+                bufs[b][0].copy_(host_batches[i][0], non_blocking=True)
+                bufs[b][1].copy_(host_batches[i][1], non_blocking=True)
+                ready[b].record(copy)
+
+        prefetch(0)
+        for i in range(k):
+            if i + 1 < k:
+                prefetch(i + 1)
+            b = i % 2
+            main.wait_event(ready[b])
+            loss = self.step(bufs[b][0], bufs[b][1])
+            free[b] = torch.cuda.Event()
+            free[b].record(main)
+            losses[i].copy_(loss.view(()), non_blocking=True)
+        return losses
+
     def step(self, rays: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
         """rays [n][6] f32, target [n][3] f32 on this rank's device; returns the local loss (device f64)."""
         n = rays.shape[0]

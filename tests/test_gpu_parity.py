@@ -542,3 +542,31 @@ def test_optimizer_descends_on_fixed_batch(env, c0_tree):
     losses = [opt.step(rays, target).item() for _ in range(8)]
     assert all(b < a for a, b in zip(losses, losses[1:])), losses
     assert losses[-1] < 0.8 * losses[0], losses
+
+
+def test_train_from_host_matches_step(env, c0_tree):
+    """OctreeOptimizer.train_from_host (side-stream H2D prefetch, async loss D2H) takes the same
+    steps as calling step() on device copies one by one: same losses and leaves up to the
+    atomic summation order."""
+    po, om, torch = env
+    from paper_2103_14024_b200.optim import OctreeOptimizer
+    cams = np.concatenate([gen.orbit_camera(3.0, 30.0 * i, 20.0, 64, 64, 70.0) for i in range(6)])
+    gt = po.tree_from_gen(c0_tree)
+    rays = po.po_camera_rays(po.cams_tensor(cams), 64, 64).reshape(-1, 6)
+    target = po.po_render_rays(gt, rays, gamma=0.0)
+    g = rng(81)
+    sig = (c0_tree.sigma + g.normal(0.0, 0.5, c0_tree.sigma.shape)).astype(np.float32)
+    sh = (c0_tree.sh + g.normal(0.0, 0.3, c0_tree.sh.shape)).astype(np.float32)
+    perm = [torch.from_numpy(rng(90 + i).permutation(rays.shape[0])[:8192]).cuda() for i in range(4)]
+    batches = [(rays[p].contiguous(), target[p].contiguous()) for p in perm]
+    trees = [po.po_tree_create(c0_tree.child, sig, sh, c0_tree.depth, 1, c0_tree.bbox_min, c0_tree.edge)
+             for _ in range(2)]
+    a = OctreeOptimizer(trees[0], lr=1.0, gamma=0.0)
+    ref = [a.step(r, t).item() for r, t in batches]
+    b = OctreeOptimizer(trees[1], lr=1.0, gamma=0.0)
+    host = [(r.cpu().pin_memory(), t.cpu().pin_memory()) for r, t in batches]
+    got = b.train_from_host(host)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(got.numpy(), ref, rtol=1e-5)
+    for x, y in zip(trees[0].read_leaves(), trees[1].read_leaves()):
+        np.testing.assert_allclose(x, y, rtol=1e-4, atol=1e-5)
