@@ -1251,16 +1251,28 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
                           unsigned long long* timeline, cudaStream_t s) {
     const int64_t tiles = (int64_t)((W + 7) / 8) * ((H + 3) / 4) * n_cams;
     if (tiles >= (int64_t)0xFFFFFFF0u) return cudaErrorInvalidValue;
-    // CTAs per SM the register budget is tuned for.  Default 2 (<= 128 registers): all 12
-    // LDG.128 of a leaf row stay in flight, which beat 3-4 CTAs/SM on B200 (r01: 4127 vs 3819
-    // vs 3160 FPS on c1).  For the SH-3 fp32 path PO_RENDER_MINB=1,3,4 and PO_RENDER_OPT
-    // (0 = the plain neighbour step, 64 = traversal-only probe; traverse.cuh) select other
-    // instances for A/B experiments.
-    static const int minb = [] {
+    // CTAs per SM the register budget is tuned for (SH-3 paths), chosen by the work per launch.
+    // A single view is bounded by its slowest warp tiles: 2 CTAs/SM (<= 128
+    // registers, all 12 LDG.128 of a leaf row in flight) gives those tiles the most issue slots
+    // (c1: 4441 vs 3979 FPS at 3/SM).  With several views per launch the slow tiles overlap
+    // other views and throughput wins: 3/SM from 2 views on (8 views: 7537 vs 6719 views/s),
+    // 4/SM for very large launches (c2, 200 views: 8881 vs 8544 vs 7245 views/s at 4/3/2).
+    // Rule in warp tiles per SM: < 200 -> 2, < 4000 -> 3, else 4.  PO_RENDER_MINB=1..4
+    // overrides it; PO_RENDER_OPT (0 = plain neighbour step, 64 = traversal-only probe;
+    // traverse.cuh) selects SH-3 fp32 variants for A/B experiments.
+    static const int env_minb = [] {
         const char* e = getenv("PO_RENDER_MINB");
-        const int v = e ? atoi(e) : 2;
-        return (v >= 1 && v <= 4) ? v : 2;
+        const int v = e ? atoi(e) : 0;
+        return (v >= 1 && v <= 4) ? v : 0;
     }();
+    static const int n_sm = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            v = 148;
+        return v > 0 ? v : 148;
+    }();
+    const int64_t tiles_per_sm = tiles / n_sm;
+    const int minb = env_minb ? env_minb : (tiles_per_sm < 200 ? 2 : (tiles_per_sm < 4000 ? 3 : 4));
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
@@ -1269,15 +1281,17 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
                          unsigned long long*);
     KFn fn = nullptr;
-    if (deg == 3 && !f16 && (minb != 2 || vopt != kRenderOptDefault)) {
-        static const KFn by_minb[4] = {k_render<3, false, 1, kRenderOptDefault>, k_render<3, false, 2, kRenderOptDefault>,
-                                       k_render<3, false, 3, kRenderOptDefault>,
-                                       k_render<3, false, 4, kRenderOptDefault>};
+    if (deg == 3 && vopt == kRenderOptDefault) {
+        static const KFn k32[4] = {k_render<3, false, 1, kRenderOptDefault>, k_render<3, false, 2, kRenderOptDefault>,
+                                   k_render<3, false, 3, kRenderOptDefault>, k_render<3, false, 4, kRenderOptDefault>};
+        static const KFn k16[4] = {k_render<3, true, 1, kRenderOptDefault>, k_render<3, true, 2, kRenderOptDefault>,
+                                   k_render<3, true, 3, kRenderOptDefault>, k_render<3, true, 4, kRenderOptDefault>};
+        fn = f16 ? k16[minb - 1] : k32[minb - 1];
+    } else if (deg == 3 && !f16) {
         static const KFn probe[4] = {k_render<3, false, 1, kOptProbeNoShade>, k_render<3, false, 2, kOptProbeNoShade>,
                                      k_render<3, false, 3, kOptProbeNoShade>, k_render<3, false, 4, kOptProbeNoShade>};
         if (vopt == kOptProbeNoShade) fn = probe[minb - 1];
-        else if (vopt == kOptPlain && minb == 2) fn = k_render<3, false, 2, kOptPlain>;
-        else fn = by_minb[minb - 1];
+        else fn = k_render<3, false, 2, kOptPlain>;
     } else {
         PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kRenderOptDefault>);
     }
