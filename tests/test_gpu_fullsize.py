@@ -90,3 +90,21 @@ def test_c1_backward_ray_subset(env, c1_tree):
     mask = np.ones(gs.shape[0], bool)
     mask[touched] = False
     assert not gs[mask].any() and not gk[mask].any()
+
+
+@pytest.mark.parametrize("payload", ["f32", "f16"])
+def test_multi_view_launch_instances_match_single_views(env, c1_tree, payload):
+    """The render picks its CTAs-per-SM instance by the work per launch (2 for one 800x800 view,
+    3 for 4 views, 4 for 32 views; launch_render).  Every instance must give the single-view
+    image bit for bit: views of a 4- and a 32-view launch against one-view launches."""
+    po, om, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    if payload == "f16":
+        tree = po.po_tree_convert(tree, po.PO_F16)
+    cams = po.cams_tensor(np.concatenate([gen.config_camera("c2", 7 * v)[0] for v in range(32)]))
+    single = {v: po.po_render(tree, cams[v:v + 1], 800, 800) for v in (0, 3, 17, 31)}
+    four = po.po_render(tree, cams[:4], 800, 800)
+    assert torch.equal(four[0], single[0][0]) and torch.equal(four[3], single[3][0])
+    many = po.po_render(tree, cams, 800, 800)
+    for v in (0, 3, 17, 31):
+        assert torch.equal(many[v], single[v][0]), v
