@@ -143,7 +143,11 @@ po_status po_render_shard(const po_tree* tree, const po_camera* cams, int32_t n_
  * renders, copies the image out and synchronises the stream (end-to-end entry point).  If
  * out_rgb_host is pinned (cudaHostAlloc / torch pin_memory: device-mapped under unified
  * addressing) the kernel writes the pixels straight into it over PCIe while rendering
- * (PO_HOST_DIRECT=0 forces the staged copy); pageable memory is staged and copied. */
+ * (PO_HOST_DIRECT=0 forces the staged copy); pageable memory is staged and copied.  A single
+ * view's camera is passed by value (no camera copy).  A pinned buffer of more than 12 MiB with
+ * 4 or more views is filled by a chunk pipeline instead: chunks of views rendered into device
+ * buffers owned by the tree, each copied out on a second stream while the next one renders
+ * (PO_HOST_PIPE=0 disables it).  Calls on one tree are serialised for that pipeline. */
 po_status po_render_host(const po_tree* tree, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
                          const po_render_opts* opts, float* out_rgb_host, po_stream stream);
 

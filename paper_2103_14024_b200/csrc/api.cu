@@ -32,6 +32,13 @@ struct po_tree {
     int cam_cap = 0;
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
+    // po_render_host's chunked pipeline (multi-view renders into pinned buffers): two device
+    // chunk buffers, a copy stream and its events, used under pipe_mu
+    float* d_pipe = nullptr;
+    size_t pipe_cap = 0;
+    cudaStream_t pipe_stream = nullptr;
+    cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // rendered[2], copied[2]
+    std::mutex pipe_mu;
     // centre-out order of the 16x16 pixel blocks of a W x H view (built once per size)
     unsigned* d_order = nullptr;
     int order_w = 0, order_h = 0;
@@ -425,6 +432,10 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_cams) cudaFree(t->d_cams);
     if (t->d_work) cudaFree(t->d_work);
     if (t->d_img) cudaFree(t->d_img);
+    if (t->d_pipe) cudaFree(t->d_pipe);
+    for (cudaEvent_t ev : t->pipe_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (t->pipe_stream) cudaStreamDestroy(t->pipe_stream);
     if (t->d_order) cudaFree(t->d_order);
     if (t->d_order_zip) cudaFree(t->d_order_zip);
     if (t->d_plan) cudaFree(t->d_plan);
@@ -580,6 +591,58 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
             direct = static_cast<float*>(pa.devicePointer);
         else
             (void)cudaGetLastError();   // pageable memory: not an error
+    }
+    // Multi-view renders into a pinned buffer whose transfer outlasts the render (c2: 200 views,
+    // 1.5 GB): the copy engine moves data faster than SM stores into host memory (55.7 vs 47-50
+    // GB/s, tools/micro/hostwrite.cu), so views are rendered in chunks into device buffers and
+    // each chunk's D2H copy runs on a second stream while the next chunk renders.
+    static const bool pipe_ok = [] {
+        const char* ev = getenv("PO_HOST_PIPE");
+        return !(ev && std::strcmp(ev, "0") == 0);
+    }();
+    if (direct && pipe_ok && n_cams >= 4 && out_bytes > ((size_t)12 << 20)) {
+        std::lock_guard<std::mutex> lk(t->pipe_mu);
+        const int chunk = n_cams >= 32 ? 16 : (n_cams + 1) / 2;   // views per render launch
+        const size_t view_floats = (size_t)W * H * 3;
+        const size_t cfloats = (size_t)chunk * view_floats;
+        if (t->pipe_stream == nullptr) {
+            if ((e = cudaStreamCreateWithFlags(&t->pipe_stream, cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_status(e, "copy stream");
+            for (cudaEvent_t& ev : t->pipe_ev)
+                if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+                    return cuda_status(e, "copy events");
+        }
+        if (t->pipe_cap < 2 * cfloats) {
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess || (e = cudaStreamSynchronize(t->pipe_stream)) != cudaSuccess)
+                return cuda_status(e, "sync");
+            if (t->d_pipe) cudaFree(t->d_pipe);
+            t->d_pipe = nullptr;
+            t->pipe_cap = 0;
+            if ((e = cudaMalloc((void**)&t->d_pipe, 2 * cfloats * sizeof(float))) != cudaSuccess)
+                return cuda_status(e, "cudaMalloc(chunk buffers)");
+            t->pipe_cap = 2 * cfloats;
+        }
+        po_status st = PO_OK;
+        for (int k = 0, v0 = 0; v0 < n_cams && st == PO_OK; ++k, v0 += chunk) {
+            const int nv = std::min(chunk, n_cams - v0), b = k & 1;
+            float* buf = t->d_pipe + (size_t)b * cfloats;
+            if (k >= 2 && (e = cudaStreamWaitEvent(s, t->pipe_ev[2 + b], 0)) != cudaSuccess) {   // buffer copied out
+                st = cuda_status(e, "wait copy");
+                break;
+            }
+            st = render_scheduled(t, t->d_cams + v0, nv, W, H, o, buf, s, "po_render_host");
+            if (st != PO_OK) break;
+            if ((e = cudaEventRecord(t->pipe_ev[b], s)) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(t->pipe_stream, t->pipe_ev[b], 0)) != cudaSuccess ||
+                (e = cudaMemcpyAsync(out_host + (size_t)v0 * view_floats, buf, (size_t)nv * view_floats * sizeof(float),
+                                     cudaMemcpyDeviceToHost, t->pipe_stream)) != cudaSuccess ||
+                (e = cudaEventRecord(t->pipe_ev[2 + b], t->pipe_stream)) != cudaSuccess)
+                st = cuda_status(e, "chunk copy");
+        }
+        cudaError_t e1 = cudaStreamSynchronize(t->pipe_stream), e2 = cudaStreamSynchronize(s);
+        if (st == PO_OK && e1 != cudaSuccess) st = cuda_status(e1, "sync");
+        if (st == PO_OK && e2 != cudaSuccess) st = cuda_status(e2, "sync");
+        return st;
     }
     if (direct) {
         // Block order for in-kernel image stores over PCIe (GPU stores into mapped pinned memory

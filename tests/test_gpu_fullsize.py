@@ -108,3 +108,18 @@ def test_multi_view_launch_instances_match_single_views(env, c1_tree, payload):
     many = po.po_render(tree, cams, 800, 800)
     for v in (0, 3, 17, 31):
         assert torch.equal(many[v], single[v][0]), v
+
+
+@pytest.mark.parametrize("n_views", [6, 34])
+def test_host_render_chunk_pipeline(env, c1_tree, n_views):
+    """po_render_host into a pinned buffer of more than 12 MiB with several views renders in
+    chunks (3 / 16 views) into device buffers whose D2H copies overlap the next chunk; the host
+    image must equal the device render bit for bit (34 views: chunks of 16, 16 and 2)."""
+    po, om, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    recs = np.concatenate([gen.config_camera("c2", 5 * v)[0] for v in range(n_views)])
+    dev = po.po_render(tree, po.cams_tensor(recs), 800, 800).cpu()
+    pinned = torch.empty((n_views, 800, 800, 3), dtype=torch.float32, pin_memory=True)
+    pinned.fill_(-1.0)
+    po.po_render_host(tree, recs, 800, 800, out_host=pinned.numpy())
+    assert torch.equal(pinned, dev)
