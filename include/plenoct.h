@@ -147,7 +147,10 @@ po_status po_render_shard(const po_tree* tree, const po_camera* cams, int32_t n_
  * view's camera is passed by value (no camera copy).  A pinned buffer of more than 12 MiB with
  * 4 or more views is filled by a chunk pipeline instead: chunks of views rendered into device
  * buffers owned by the tree, each copied out on a second stream while the next one renders
- * (PO_HOST_PIPE=0 disables it).  Calls on one tree are serialised for that pipeline. */
+ * (PO_HOST_PIPE=0 disables it).  A single view of more than 12 MiB is rendered into a device
+ * image whose bands of block rows are copied out as the kernel completes them (stream
+ * memory-operation waits on per-band counters; PO_HOST_BANDS=0 disables it).  Calls on one tree
+ * are serialised for these pipelines. */
 po_status po_render_host(const po_tree* tree, const po_camera* cams_host, int32_t n_cams, int32_t W, int32_t H,
                          const po_render_opts* opts, float* out_rgb_host, po_stream stream);
 

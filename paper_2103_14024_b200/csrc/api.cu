@@ -2,6 +2,7 @@
 // device selection and kernel launches.  No compute happens here; there is no CPU path.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cuda.h>   // driver API types only (cuStreamWaitValue64 comes via cudaGetDriverEntryPoint)
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -39,6 +40,10 @@ struct po_tree {
     cudaStream_t pipe_stream = nullptr;
     cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // rendered[2], copied[2]
     std::mutex pipe_mu;
+    // po_render_host band pipeline (one view): cumulative per-band tile counters for W x H
+    unsigned long long* d_band = nullptr;
+    int band_w = 0, band_h = 0;
+    unsigned long long band_calls = 0;
     // centre-out order of the 16x16 pixel blocks of a W x H view (built once per size)
     unsigned* d_order = nullptr;
     int order_w = 0, order_h = 0;
@@ -433,6 +438,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->d_work) cudaFree(t->d_work);
     if (t->d_img) cudaFree(t->d_img);
     if (t->d_pipe) cudaFree(t->d_pipe);
+    if (t->d_band) cudaFree(t->d_band);
     for (cudaEvent_t ev : t->pipe_ev)
         if (ev) cudaEventDestroy(ev);
     if (t->pipe_stream) cudaStreamDestroy(t->pipe_stream);
@@ -503,9 +509,9 @@ static po_status check_cams_host(const po_camera* c, int32_t n) {
 // (An order by measured or probed block cost was tried in r01 and was slower: DESIGN.md §6.1.)
 static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams, int W, int H,
                                   const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
-                                  unsigned long long* timeline = nullptr, bool zip = false) {
+                                  unsigned long long* timeline = nullptr, bool zip = false, bool raster = false) {
     cudaError_t e = cudaSuccess;
-    const unsigned* order = block_order(t, W, H, s, &e, zip);
+    const unsigned* order = raster ? nullptr : block_order(t, W, H, s, &e, zip);
     if (e != cudaSuccess) return cuda_status(e, "block order");
     const int slot = t->next_slot();
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
@@ -638,6 +644,100 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
                                      cudaMemcpyDeviceToHost, t->pipe_stream)) != cudaSuccess ||
                 (e = cudaEventRecord(t->pipe_ev[2 + b], t->pipe_stream)) != cudaSuccess)
                 st = cuda_status(e, "chunk copy");
+        }
+        cudaError_t e1 = cudaStreamSynchronize(t->pipe_stream), e2 = cudaStreamSynchronize(s);
+        if (st == PO_OK && e1 != cudaSuccess) st = cuda_status(e1, "sync");
+        if (st == PO_OK && e2 != cudaSuccess) st = cuda_status(e2, "sync");
+        return st;
+    }
+    // One large view into a pinned buffer: render into a device image in raster block order and let a
+    // copy stream move each band of block rows as soon as its last tile is stored (the kernel
+    // counts stored tiles per band; cuStreamWaitValue64 gates each band's D2H copy), so the
+    // copy engine (55.7 GB/s) streams the image while the rest renders and only the last band's
+    // copy follows the kernel.  Needs 64-bit stream memory operations; PO_HOST_BANDS=0 (or no
+    // support) keeps the in-kernel stores below.
+    using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+    static const WaitFn wait64 = []() -> WaitFn {
+        const char* ev = getenv("PO_HOST_BANDS");
+        if (ev && std::strcmp(ev, "0") == 0) return nullptr;
+        void* fp = nullptr;
+        void* ga = nullptr;
+        cudaDriverEntryPointQueryResult q1, q2;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fp, cudaEnableDefault, &q1) != cudaSuccess ||
+            q1 != cudaDriverEntryPointSuccess ||
+            cudaGetDriverEntryPoint("cuDeviceGetAttribute", &ga, cudaEnableDefault, &q2) != cudaSuccess ||
+            q2 != cudaDriverEntryPointSuccess) {
+            (void)cudaGetLastError();
+            return nullptr;
+        }
+        int dev = 0, ok = 0;
+        cudaGetDevice(&dev);
+        using AttrFn = CUresult (*)(int*, CUdevice_attribute, CUdevice);
+        if (reinterpret_cast<AttrFn>(ga)(&ok, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, dev) != CUDA_SUCCESS ||
+            !ok)
+            return nullptr;
+        return reinterpret_cast<WaitFn>(fp);
+    }();
+    // Only for images above 12 MiB: a smaller image moves faster than it renders, and its last
+    // bands (the costly centre rows finish last) would be copied after the kernel -- in-kernel
+    // stores win there (c1 800x800: 3700 vs 2545 FPS end to end; c3 1920x1080: 1878 vs 1126).
+    if (direct && n_cams == 1 && wait64 != nullptr && out_bytes > ((size_t)12 << 20)) {
+        std::lock_guard<std::mutex> lk(t->pipe_mu);
+        const int by_n = (H + 15) / 16, bx_n = (W + 15) / 16;
+        const int band_rows = (by_n + 7) / 8;   // 8 bands
+        const int nb = (by_n + band_rows - 1) / band_rows;
+        if (t->pipe_stream == nullptr) {
+            if ((e = cudaStreamCreateWithFlags(&t->pipe_stream, cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_status(e, "copy stream");
+            for (cudaEvent_t& ev : t->pipe_ev)
+                if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+                    return cuda_status(e, "copy events");
+        }
+        if (t->d_band == nullptr || t->band_w != W || t->band_h != H) {   // counters restart at 0
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess || (e = cudaStreamSynchronize(t->pipe_stream)) != cudaSuccess)
+                return cuda_status(e, "sync");
+            if (t->d_band) cudaFree(t->d_band);
+            t->d_band = nullptr;
+            if ((e = cudaMalloc((void**)&t->d_band, 8 * sizeof(unsigned long long))) != cudaSuccess)
+                return cuda_status(e, "cudaMalloc(band counters)");
+            if ((e = cudaMemset(t->d_band, 0, 8 * sizeof(unsigned long long))) != cudaSuccess)
+                return cuda_status(e, "memset(band counters)");
+            t->band_w = W;
+            t->band_h = H;
+            t->band_calls = 0;
+        }
+        if (t->img_cap < out_bytes) {
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess || (e = cudaStreamSynchronize(t->pipe_stream)) != cudaSuccess)
+                return cuda_status(e, "sync");
+            if (t->d_img) cudaFree(t->d_img);
+            t->d_img = nullptr;
+            t->img_cap = 0;
+            if ((e = cudaMalloc((void**)&t->d_img, out_bytes)) != cudaSuccess) return cuda_status(e, "cudaMalloc(image)");
+            t->img_cap = out_bytes;
+        }
+        // the copies of the previous call on this tree are done with d_img before it is rewritten
+        if ((e = cudaEventRecord(t->pipe_ev[2], t->pipe_stream)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(s, t->pipe_ev[2], 0)) != cudaSuccess)
+            return cuda_status(e, "order");
+        const unsigned long long call = ++t->band_calls;
+        po::RenderOpts ob = o;
+        ob.band_done = t->d_band;
+        ob.band_rows = band_rows;
+        po_status st = render_scheduled(t, t->d_cams, 1, W, H, ob, t->d_img, s, "po_render_host", nullptr, false, true);
+        const size_t row_floats = (size_t)W * 3;
+        for (int b = 0; b < nb && st == PO_OK; ++b) {
+            const int br0 = b * band_rows, br1 = std::min(by_n, br0 + band_rows);
+            const int r0 = br0 * 16, r1 = std::min(H, br1 * 16);
+            const cuuint64_t target = (cuuint64_t)call * (cuuint64_t)bx_n * (br1 - br0) * 8;   // 8 tiles per block
+            CUresult ce = wait64((CUstream)t->pipe_stream, (CUdeviceptr)(t->d_band + b), target, CU_STREAM_WAIT_VALUE_GEQ);
+            if (ce != CUDA_SUCCESS) {
+                st = fail(PO_ERR_CUDA, "cuStreamWaitValue64 failed (%d)", (int)ce);
+                break;
+            }
+            if ((e = cudaMemcpyAsync(out_host + (size_t)r0 * row_floats, t->d_img + (size_t)r0 * row_floats,
+                                     (size_t)(r1 - r0) * row_floats * sizeof(float), cudaMemcpyDeviceToHost,
+                                     t->pipe_stream)) != cudaSuccess)
+                st = cuda_status(e, "band copy");
         }
         cudaError_t e1 = cudaStreamSynchronize(t->pipe_stream), e2 = cudaStreamSynchronize(s);
         if (st == PO_OK && e1 != cudaSuccess) st = cuda_status(e1, "sync");

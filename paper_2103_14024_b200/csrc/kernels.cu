@@ -426,6 +426,11 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             }
         }
         store_tile_rgb(out, (size_t)view * H, W, H, bx * 16 + (int)(sub & 1u) * 8, by * 16 + (int)(sub >> 1) * 4, C);
+        if (opt.band_done != nullptr) {   // this tile's pixels are stored: count it for its band
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(opt.band_done + by / opt.band_rows, 1ull);
+        }
         if (timeline != nullptr) {   // measurement mode (po_render_timeline): one record per warp tile
             __syncwarp();
             if (lane == 0) {

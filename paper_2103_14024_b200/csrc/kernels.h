@@ -17,6 +17,10 @@ struct RenderOpts {
     // k_render only: one view's camera by value (cams unused), so a host camera needs no copy
     int32_t cam_inline = 0;
     float cam[16] = {};
+    // k_render only (po_render_host band pipeline): after each warp tile's store, add 1 to
+    // band_done[block_row / band_rows] (cumulative 64-bit counters a copy stream waits on)
+    unsigned long long* band_done = nullptr;
+    int32_t band_rows = 0;
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.

@@ -123,3 +123,18 @@ def test_host_render_chunk_pipeline(env, c1_tree, n_views):
     pinned.fill_(-1.0)
     po.po_render_host(tree, recs, 800, 800, out_host=pinned.numpy())
     assert torch.equal(pinned, dev)
+
+
+def test_host_render_band_pipeline(env, c1_tree):
+    """po_render_host of ONE view into a pinned buffer copies bands of block rows out as the
+    kernel finishes them (per-band tile counters gating cuStreamWaitValue64 on a copy stream).
+    Repeated calls (cumulative counters) and a size change must each give the device image."""
+    po, om, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    for k, (W, H) in enumerate([(800, 800), (800, 800), (1920, 1080), (800, 800), (37, 23)]):
+        rec = gen.orbit_camera(3.4, 40.0 + 9.0 * k, 25.0, W, H, 1111.1)
+        dev = po.po_render(tree, po.cams_tensor(rec), W, H).cpu()
+        pinned = torch.empty((1, H, W, 3), dtype=torch.float32, pin_memory=True)
+        pinned.fill_(-1.0)
+        po.po_render_host(tree, rec, W, H, out_host=pinned.numpy())
+        assert torch.equal(pinned, dev), (k, W, H)
