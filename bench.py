@@ -45,9 +45,9 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _ncu_traffic():
-    """dram bytes per k_render launch from the committed ncu --set full summary, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_render_summary.json")
+def _ncu_traffic(wl: str = "c1"):
+    """dram bytes per k_render launch of workload wl from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_render_summary.json" if wl == "c1" else f"ncu_render_summary_{wl}.json")
     try:
         with open(path) as f:
             s = json.load(f)
@@ -294,7 +294,8 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = _peaks()
         achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-        traffic, tsrc = _ncu_traffic() if wl == "c1" else (None, None)
+        traffic, tsrc = (_ncu_traffic(wl) if (wl != "c2" and V == 1) or (wl == "c2" and ws == 1)
+                         else (None, None))   # the captured launch shape only
         line = {
             "metric": metric, "value": round(fps, 2), "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,

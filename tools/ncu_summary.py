@@ -4,7 +4,8 @@
 usage: python tools/ncu_summary.py <tag> [launches.csv] [prof.ncu-rep] [kernel]
 writes profiles/<tag>_launches.md (per-kernel device time and share of the bench run),
 profiles/<tag>_<kernel>_ncu.md (key --set full metrics) and, for k_render,
-profiles/ncu_render_summary.json (dram bytes per launch, read by bench.py as `traffic`).
+profiles/ncu_render_summary.json (dram bytes per launch, read by bench.py as `traffic`;
+NCU_WORKLOAD=c2|c3 writes profiles/ncu_render_summary_<wl>.json instead).
 """
 import csv
 import json
@@ -99,9 +100,12 @@ def main():
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             by = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
-            json.dump({"dram_bytes_per_launch": by, "source": f"profiles/{tag}_{kern}_ncu.md (ncu --set full, one c1 frame, cold L2)",
+            wl = os.environ.get("NCU_WORKLOAD", "c1")   # which bench workload the capture is of
+            what = {"c1": "one c1 frame", "c2": "one c2 launch (200 views)", "c3": "one c3 frame"}.get(wl, wl)
+            name = "ncu_render_summary.json" if wl == "c1" else f"ncu_render_summary_{wl}.json"
+            json.dump({"dram_bytes_per_launch": by, "source": f"profiles/{tag}_{kern}_ncu.md (ncu --set full, {what}, cold L2)",
                        "duration": d["gpu__time_duration.sum"]},
-                      open(os.path.join(ROOT, "profiles", "ncu_render_summary.json"), "w"), indent=1)
+                      open(os.path.join(ROOT, "profiles", name), "w"), indent=1)
 
 
 if __name__ == "__main__":
