@@ -824,8 +824,10 @@ po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const p
     if (!rays || !out_rgb) return fail(PO_ERR_INVALID_ARG, "rays / out_rgb NULL");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    po_tree* tm = const_cast<po_tree*>(t);   // only the work counters are mutated
     return launched(po::launch_render_rays(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, o,
-                                           out_rgb, aux, leaf_span, sg, (cudaStream_t)stream),
+                                           out_rgb, aux, leaf_span, sg, (cudaStream_t)stream,
+                                           tm->work_of(tm->next_slot())),
                     "po_render_rays");
 }
 

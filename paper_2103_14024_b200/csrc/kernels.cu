@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -457,13 +458,11 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
     }
 }
 
+// One ray of po_render_rays (forward, or pass 1 with aux / leaf span / stored segments).
 template <int DEG, bool F16>
-__global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
-                                                     RenderOpts opt, float* __restrict__ out, double* __restrict__ aux,
-                                                     uint32_t* __restrict__ span, SegOut so) {
-    PO_DECLARE_STACK(stk);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+__device__ __forceinline__ void render_ray(const DevTree& tr, const float* __restrict__ rays, int64_t i,
+                                           const RenderOpts& opt, float* __restrict__ out, double* __restrict__ aux,
+                                           uint32_t* __restrict__ span, const SegOut& so, const SmemStack& stk) {
     float o[3], d[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -510,6 +509,46 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float*
         aux[i * 4 + 3] = (double)T;
         if (span != nullptr) reinterpret_cast<uint2*>(span)[i] = make_uint2(lo, hi);
         if (so.count != nullptr) so.count[i] = nseg;
+    }
+}
+
+template <int DEG, bool F16>
+__global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                     RenderOpts opt, float* __restrict__ out, double* __restrict__ aux,
+                                                     uint32_t* __restrict__ span, SegOut so) {
+    PO_DECLARE_STACK(stk);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    render_ray<DEG, F16>(tr, rays, i, opt, out, aux, span, so, stk);
+}
+
+// Persistent variant: every warp claims the next 32 consecutive rays from a global counter, so
+// a warp slot is refilled as soon as its own rays finish (a one-thread-per-ray grid holds each
+// CTA's slot until its slowest warp ends: at gamma = 0 the ray lengths vary widely).  work[0] =
+// next chunk, work[1] = finished CTAs; both zero on entry, reset by the last CTA.
+template <int DEG, bool F16>
+__global__ void __launch_bounds__(256, 2) k_render_rays_p(DevTree tr, const float* __restrict__ rays, int64_t n,
+                                                       RenderOpts opt, float* __restrict__ out,
+                                                       double* __restrict__ aux, uint32_t* __restrict__ span,
+                                                       SegOut so, unsigned* __restrict__ work) {
+    PO_DECLARE_STACK(stk);
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned c = 0;
+        if (lane == 0) c = atomicAdd(work, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const int64_t i0 = (int64_t)c * 32;
+        if (i0 >= n) break;
+        if (i0 + lane < n) render_ray<DEG, F16>(tr, rays, i0 + lane, opt, out, aux, span, so, stk);
+        __syncwarp();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            atomicExch(work, 0u);
+            atomicExch(work + 1, 0u);
+        }
     }
 }
 
@@ -1317,7 +1356,7 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
 
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
                                const RenderOpts& opt, float* out, double* aux, uint32_t* span, const Segments& sg,
-                               cudaStream_t s) {
+                               cudaStream_t s, unsigned* work) {
     if (n == 0) return cudaSuccess;
     const SegOut so{static_cast<float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
     static const int dopt = [] {   // measurement variants (k_render_rays_diag)
@@ -1329,6 +1368,19 @@ cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float
             k_render_rays_diag<kOptProbeNoShade><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out);
         else
             k_render_rays_diag<kOptLean><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, opt, out);
+        return cudaGetLastError();
+    }
+    static const bool persist = [] {   // A/B: PO_RAYS_PERSIST=0 keeps one thread per ray
+        const char* e = getenv("PO_RAYS_PERSIST");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (persist && work != nullptr && (n + 31) / 32 < (int64_t)0xFFFFFFF0u) {
+        PO_DISPATCH(deg, f16, {
+            static const int grid = persistent_grid(k_render_rays_p<DEG, F16>, 1 << 30, 0);
+            const int64_t need = (n + 255) / 256;
+            k_render_rays_p<DEG, F16><<<(unsigned)(grid < need ? grid : need), 256, 0, s>>>(tr, rays, n, opt, out, aux,
+                                                                                          span, so, work);
+        });
         return cudaGetLastError();
     }
     PO_DISPATCH(deg, f16, {

@@ -43,7 +43,7 @@ struct Segments {
 };
 cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float* rays, int64_t n,
                                const RenderOpts& opt, float* out, double* aux, uint32_t* span, const Segments& sg,
-                               cudaStream_t s);
+                               cudaStream_t s, unsigned* work = nullptr);   // work: 2 zeroed counters -> persistent
 cudaError_t launch_backward_chunk(const DevTree& tr, int deg, bool f16, const float* rays, const int32_t* perm,
                                   const int64_t* chunk_end, int chunk, const float* dL_dC, const double* aux,
                                   const Segments& sg, const RenderOpts& opt, float* grad_sigma, float* grad_sh,
