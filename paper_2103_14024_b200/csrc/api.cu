@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <cstdarg>
 #include <cstdlib>
@@ -59,6 +60,8 @@ struct po_tree {
     int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
     unsigned* work_of(int slot) { return d_work + 2 * slot; }
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
+    uint32_t* d_grid = nullptr;      // k_render's dense level-(D-1) cell index (build_grid)
+    bool grid_tried = false;
     static constexpr int64_t kPayloadPad = 4096;   // spare zero leaves after the payload arrays
     float4* d_sg = nullptr;          // spherical-Gaussian lobes (po_tree_set_sg_basis) or null
     std::vector<float> h_sg;         // the same on the host, [B][4]
@@ -153,8 +156,52 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
     return d_ord;
 }
 
+// The level-(D-1) cell index of k_render (kOptGrid): for every cell of the 2^(D-1)-per-axis grid
+// the entry of the depth-(D-1) node covering it, a depth-(D-1) leaf's entry, or the level of the
+// empty box containing it (0xFFFFFFFF: a coarser leaf, traversed the classic way).  Built on the
+// host from the caller's child table at the first render of the tree (D in 2..10; 67 MB at
+// D = 9, 537 MB at D = 10), read-only afterwards.  Caller holds order_mu.
+static void build_grid(po_tree* t) {
+    const int D = t->desc.max_depth;
+    if (t->d_grid || D < 1 || D > 10) return;
+    const int G2 = 1 << (D - 1);
+    std::vector<uint32_t> g((size_t)G2 * G2 * G2, 0u);
+    auto fill = [&](int x0, int y0, int z0, int n, uint32_t v) {   // grid cells [x0, x0+n)^3
+        for (int x = x0; x < x0 + n; ++x)
+            for (int y = y0; y < y0 + n; ++y)
+                for (int z = z0; z < z0 + n; ++z) g[((size_t)x * G2 + y) * G2 + z] = v;
+    };
+    // node at `level` with its box corner in grid cells (level-(D-1) units), box edge 2^(D-1-level)
+    std::function<void(uint32_t, int, int, int, int)> rec = [&](uint32_t node, int level, int x0, int y0, int z0) {
+        const int half = 1 << (D - 2 - level);   // child edge in grid cells (level < D-1 here)
+        for (int oct = 0; oct < 8; ++oct) {
+            const uint32_t e = t->h_child[(size_t)node * 8 + oct];
+            const int cx = x0 + ((oct >> 2) & 1) * half, cy = y0 + ((oct >> 1) & 1) * half, cz = z0 + (oct & 1) * half;
+            const uint32_t tag = e >> 30;
+            if (tag == 1u) {
+                if (level + 1 == D - 1) g[((size_t)cx * G2 + cy) * G2 + cz] = e;
+                else rec(e & ((1u << 30) - 1u), level + 1, cx, cy, cz);
+            } else if (tag == 2u) {
+                fill(cx, cy, cz, half, level + 1 == D - 1 ? e : 0xFFFFFFFFu);
+            } else {
+                fill(cx, cy, cz, half, (uint32_t)(level + 1));   // empty box at level+1
+            }
+        }
+    };
+    if (D == 1) return;
+    rec(0u, 0, 0, 0, 0);
+    uint32_t* d = nullptr;
+    if (cudaMalloc(&d, g.size() * 4) != cudaSuccess) return;
+    if (cudaMemcpy(d, g.data(), g.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return;
+    }
+    t->d_grid = d;
+}
+
 po::DevTree dev_tree(const po_tree* t) {
     po::DevTree d;
+    d.grid = t->d_grid;
     d.child = t->d_child;
     d.sigma = t->d_sigma;
     d.sh = t->d_sh;
@@ -444,6 +491,7 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->pipe_stream) cudaStreamDestroy(t->pipe_stream);
     if (t->d_order) cudaFree(t->d_order);
     if (t->d_order_zip) cudaFree(t->d_order_zip);
+    if (t->d_grid) cudaFree(t->d_grid);
     if (t->d_plan) cudaFree(t->d_plan);
     if (t->d_det) cudaFree(t->d_det);
     if (t->d_sg) cudaFree(t->d_sg);
@@ -511,6 +559,13 @@ static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams,
                                   const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
                                   unsigned long long* timeline = nullptr, bool zip = false, bool raster = false) {
     cudaError_t e = cudaSuccess;
+    {
+        std::lock_guard<std::mutex> lk(t->order_mu);
+        if (!t->grid_tried) {   // one attempt per tree; without an index k_render descends classically
+            t->grid_tried = true;
+            build_grid(t);
+        }
+    }
     const unsigned* order = raster ? nullptr : block_order(t, W, H, s, &e, zip);
     if (e != cudaSuccess) return cuda_status(e, "block order");
     const int slot = t->next_slot();

@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                     C[0] = C[1] = C[2] = v.T;
                 } else {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-                    traverse<OPT & kOptLean>(tr, r, v, stk);
+                    traverse<OPT & (kOptLean | kOptGrid)>(tr, r, v, stk);
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -1335,6 +1335,7 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
         static const KFn probe[4] = {k_render<3, false, 1, kOptProbeNoShade>, k_render<3, false, 2, kOptProbeNoShade>,
                                      k_render<3, false, 3, kOptProbeNoShade>, k_render<3, false, 4, kOptProbeNoShade>};
         if (vopt == kOptProbeNoShade) fn = probe[minb - 1];
+        else if (vopt == kOptLean) fn = k_render<3, false, 2, kOptLean>;   // without the index
         else fn = k_render<3, false, 2, kOptPlain>;
     } else {
         PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kRenderOptDefault>);

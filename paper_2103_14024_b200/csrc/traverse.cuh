@@ -41,6 +41,9 @@ struct DevTree {
     // NEXT f3, spherical Gaussians: B lobes (unit axis xyz, bandwidth) replacing
     // the SH basis when non-null (po_tree_set_sg_basis)
     const float4* __restrict__ sg;
+    // experiment kOptGrid: entry of every level-(D-1) cell (internal node / leaf / empty box
+    // level, 0xFFFFFFFF = fall back), 2^(D-1) per axis, x-major; null when not built
+    const uint32_t* __restrict__ grid = nullptr;
 };
 
 struct RayState {
@@ -123,11 +126,16 @@ struct SmemStack {
 constexpr int kOptPlain = 0;
 constexpr int kOptProbeNoShade = 64;
 constexpr int kOptLean = 128;
+//   kOptGrid           (render experiment) boxes found through a dense level-(D-1) index:
+//                      one index load (+ one child-entry load) per step, no stack
+constexpr int kOptGrid = 8192;
 // Default traversal of every kernel (render, render_rays, backward, trace, stats), so all
 // entry points visit the same leaf segments with the same t values (po_render ==
 // po_render_rays bitwise).  Lean measured +2-3% on c1 over the plain step.
 constexpr int kOptDefault = kOptLean;
-constexpr int kRenderOptDefault = kOptDefault;
+// The frame renderer additionally finds boxes through the level-(D-1) index when the tree has
+// one (kOptGrid: same boxes, same t values, bit-identical images; DESIGN.md §6.1 v11).
+constexpr int kRenderOptDefault = kOptDefault | kOptGrid;
 
 // Optional visitor hook on_box(shift), called once per box the ray steps through (leaf or
 // empty; shift = log2 of the box edge in leaf cells).  Only the statistics visitor has it.
@@ -147,6 +155,59 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     stk[0] = kTagInternal << 30;   // the root, node 0
     int L = 0;
     vis.on_node();
+    if constexpr ((OPT & kOptGrid) != 0) {
+        if (tr.grid != nullptr && D >= 1) {
+            const int G2 = G >> 1;
+            while (true) {
+                const uint32_t E = __ldg(tr.grid + (((size_t)(c[0] >> 1) * G2 + (c[1] >> 1)) * G2 + (c[2] >> 1)));
+                uint32_t e;
+                int shift;
+                if (E == 0xFFFFFFFFu) {
+                    break;   // a coarse leaf: not indexed (never in the benchmark trees); classic path below
+                } else if ((E >> 30) == kTagInternal) {
+                    e = __ldg(tr.child + ((E & kIdxMask) * 8u + (uint32_t)(((c[0] & 1) << 2) | ((c[1] & 1) << 1) | (c[2] & 1))));
+                    shift = 0;
+                } else if ((E >> 30) == kTagLeaf) {
+                    e = E;
+                    shift = 1;
+                } else {
+                    e = 0u;
+                    shift = D - (int)(E & kIdxMask);
+                }
+                const int size = 1 << shift;
+                int lo[3];
+                float te[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    lo[k] = c[k] & ~(size - 1);
+                    const int face = (r.dg[k] >= 0.f) ? lo[k] + size : lo[k];
+                    te[k] = ((float)face - r.o[k]) * r.inv[k];
+                }
+                const float texit = fminf(fminf(te[0], te[1]), te[2]);
+                const float tout = fminf(texit, r.tfar);
+                if ((e >> 30) == kTagLeaf && tout > t) {
+                    if (!vis.on_leaf(e & kIdxMask, t, tout)) return;
+                }
+                if (!(texit < r.tfar)) return;
+                t = texit;
+                int nc[3];
+                bool out = false;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const bool hit = te[k] == texit;
+                    const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;
+                    const int ck = __float2int_rd(fmaf(t, r.dg[k], r.o[k]));
+                    nc[k] = hit ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
+                    out |= hit & ((unsigned)nex >= (unsigned)G);
+                }
+                if (out) return;
+                c[0] = nc[0];
+                c[1] = nc[1];
+                c[2] = nc[2];
+            }
+            L = 0;   // fall back from the current cell with a fresh descent
+        }
+    }
     while (true) {
         // stk[L] holds the entry word of the node at level L (the deepest common ancestor of
         // the previous and the current cell); descend to the box that contains cell c
