@@ -199,6 +199,15 @@ static void build_grid(po_tree* t) {
     t->d_grid = d;
 }
 
+// one build attempt per tree; without an index the kernels descend classically
+static void ensure_grid(po_tree* t) {
+    std::lock_guard<std::mutex> lk(t->order_mu);
+    if (!t->grid_tried) {
+        t->grid_tried = true;
+        build_grid(t);
+    }
+}
+
 po::DevTree dev_tree(const po_tree* t) {
     po::DevTree d;
     d.grid = t->d_grid;
@@ -559,13 +568,7 @@ static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams,
                                   const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
                                   unsigned long long* timeline = nullptr, bool zip = false, bool raster = false) {
     cudaError_t e = cudaSuccess;
-    {
-        std::lock_guard<std::mutex> lk(t->order_mu);
-        if (!t->grid_tried) {   // one attempt per tree; without an index k_render descends classically
-            t->grid_tried = true;
-            build_grid(t);
-        }
-    }
+    ensure_grid(t);
     const unsigned* order = raster ? nullptr : block_order(t, W, H, s, &e, zip);
     if (e != cudaSuccess) return cuda_status(e, "block order");
     const int slot = t->next_slot();
@@ -879,7 +882,8 @@ po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const p
     if (!rays || !out_rgb) return fail(PO_ERR_INVALID_ARG, "rays / out_rgb NULL");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    po_tree* tm = const_cast<po_tree*>(t);   // only the work counters are mutated
+    po_tree* tm = const_cast<po_tree*>(t);   // only the work counters and the cell index are mutated
+    ensure_grid(tm);
     return launched(po::launch_render_rays(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, o,
                                            out_rgb, aux, leaf_span, sg, (cudaStream_t)stream,
                                            tm->work_of(tm->next_slot())),

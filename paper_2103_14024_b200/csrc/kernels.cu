@@ -475,7 +475,7 @@ __device__ __forceinline__ void render_ray(const DevTree& tr, const float* __res
         float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
         if (hit) {
             FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
-            traverse(tr, r, v, stk);
+            traverse<kOptDefault | kOptGrid>(tr, r, v, stk);   // cell index when built
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
         }
@@ -493,7 +493,7 @@ __device__ __forceinline__ void render_ray(const DevTree& tr, const float* __res
                 v.seg_stride = 2 * so.n;
                 v.max_seg = so.max_seg;
             }
-            traverse(tr, r, v, stk);
+            traverse<kOptDefault | kOptGrid>(tr, r, v, stk);   // cell index when built
             nseg = v.nseg;
             T = v.T;
             lo = v.lo;
