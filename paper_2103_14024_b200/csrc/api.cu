@@ -970,6 +970,7 @@ po_status po_render_backward_chunk(const po_tree* t, const float* rays, const in
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     po_tree* mt = const_cast<po_tree*>(t);   // work counters only
     if (segments != nullptr && aux != nullptr) g_launches.fetch_add(1);   // + the replay kernel
     return launched(po::launch_backward_chunk(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, perm,
@@ -992,6 +993,7 @@ po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, con
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     if (segments != nullptr && aux != nullptr) g_launches.fetch_add(1);   // replay + overflow re-traversal
     return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
                                         sg, o, grad_sigma, grad_sh, (cudaStream_t)stream),
@@ -1015,6 +1017,7 @@ po_status po_render_backward_sgd(po_tree* t, const float* rays, int64_t n, const
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     g_launches.fetch_add(2);   // overflow re-traversal + fused replay + gated SGD
     return launched(po::launch_backward_sgd(dev_tree(t), t->desc.sh_degree, rays, n, dL_dC, aux, sg, o, t->d_sigma,
                                             static_cast<float*>(t->d_sh), t->sh_row, t->n_leaves, lr, grad_sigma,
@@ -1050,6 +1053,7 @@ po_status po_render_backward_deterministic(const po_tree* tc, const float* rays,
         return fail(PO_ERR_UNSUPPORTED, "n * max_seg >= 2^31 (32-bit segment slots)");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    ensure_grid(t);   // the cell index the overflow re-traversal reads
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     if (n_overflow && (e = cudaMemsetAsync(n_overflow, 0, sizeof(int32_t), s)) != cudaSuccess)
@@ -1180,6 +1184,7 @@ po_status po_render_depth(const po_tree* t, const float* rays, int64_t n, const 
     if (!rays || !alpha || !depth) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     return launched(po::launch_render_depth(dev_tree(t), rays, n, o.gamma, alpha, depth, (cudaStream_t)stream),
                     "po_render_depth");
 }
@@ -1194,6 +1199,7 @@ po_status po_leaf_max_alpha(const po_tree* t, const float* rays, int64_t n, cons
     if (!rays || !max_alpha) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     return launched(po::launch_leaf_max_alpha(dev_tree(t), rays, n, o.gamma, max_alpha, (cudaStream_t)stream),
                     "po_leaf_max_alpha");
 }

@@ -707,11 +707,11 @@ __device__ __forceinline__ void backward_ray(const DevTree& tr, const float* __r
         for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = aux[i * 4 + ch];
     } else {   // pass 1: total = sum_{k<=N} c_k w_k including the background
         TotalVisitor<DEG, F16> tv(tr, r.d, opt.gamma);
-        traverse(tr, r, tv, stk);
+        traverse<kOptDefault | kOptGrid>(tr, r, tv, stk);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) gv.Ctot[ch] = tv.C[ch] + (double)tv.T * (double)opt.bg[ch];
     }
-    traverse(tr, r, gv, stk);
+    traverse<kOptDefault | kOptGrid>(tr, r, gv, stk);
 }
 
 template <int DEG, bool F16, bool kSkipReplay>
@@ -1069,7 +1069,7 @@ __global__ void __launch_bounds__(256) k_render_depth(DevTree tr, const float* _
     }
     DepthVisitor v{tr, 1.f, gamma, 0.f};
     RayState r;
-    if (ray_setup(tr, o, d, r)) traverse(tr, r, v, stk);
+    if (ray_setup(tr, o, d, r)) traverse<kOptDefault | kOptGrid>(tr, r, v, stk);
     alpha[i] = __fsub_rn(1.0f, v.T);
     depth[i] = v.D;
 }
@@ -1087,7 +1087,7 @@ __global__ void __launch_bounds__(256) k_leaf_max_alpha(DevTree tr, const float*
     }
     MaxAlphaVisitor v{tr, 1.f, gamma, max_alpha};
     RayState r;
-    if (ray_setup(tr, o, d, r)) traverse(tr, r, v, stk);
+    if (ray_setup(tr, o, d, r)) traverse<kOptDefault | kOptGrid>(tr, r, v, stk);
 }
 
 __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restrict__ rays, int64_t n, float gamma,
