@@ -37,7 +37,7 @@ int main(void) {
         sigma[i] = 1.5f;
         sh[3 * i] = sh[3 * i + 1] = sh[3 * i + 2] = k;
     }
-    po_tree_desc desc = {{-1.f, -1.f, -1.f}, 2.f, 2, 0, PO_F32, PO_SH_CS, 0};
+    po_tree_desc desc = {{-1.f, -1.f, -1.f}, 2.f, 2, 0, PO_F32, PO_SH_CS, 0, 0};
     po_tree* tree = NULL;
     if (po_tree_create(&desc, child, NN, sigma, sh, NL, &tree) != PO_OK) {
         fprintf(stderr, "po_tree_create: %s\n", po_last_error());

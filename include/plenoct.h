@@ -12,6 +12,10 @@
  *  - po_stream is a cudaStream_t passed as void* (NULL = legacy default stream).  All
  *    render / backward / update calls are asynchronous on that stream; the caller
  *    orders them (e.g. po_tree_sgd_step after every render that reads the tree).
+ *  - Renders of one tree may run concurrently on different streams.  The persistent
+ *    kernels keep their work counters per (tree, stream): up to 256 distinct streams per
+ *    tree (PO_ERR_UNSUPPORTED beyond).  A destroyed stream's counters are reused only by a
+ *    stream with the same handle, i.e. after the old one's work has been ordered before it.
  *  - CUDA launch and asynchronous errors map to PO_ERR_CUDA (a sticky error from an
  *    earlier kernel is reported by the next call that checks).
  *  - There is NO CPU fallback: every compute call runs CUDA kernels for sm_100a.
@@ -50,7 +54,17 @@ typedef struct {
     int32_t payload;      /* PO_F32 | PO_F16                                   */
     int32_t sh_sign;      /* PO_SH_CS | PO_SH_NO_CS                            */
     int32_t device;       /* CUDA ordinal the tree lives on                    */
+    int32_t flags;        /* 0 or PO_TREE_NO_INDEX                             */
 } po_tree_desc;
+
+/* po_tree_desc.flags.  By default po_tree_create also builds the tree's dense level-(D-1) cell
+ * index (D in 2..10): one uint32 per cell of the 2^(D-1)-per-axis grid, 4 * 8^(D-1) bytes
+ * (67 MB at D = 9, 537 MB at D = 10; po_tree_index_bytes), through which every traversal
+ * kernel finds the box that contains a cell with one or two loads instead of a re-descent
+ * (same boxes and t values, bit-identical results).  PO_TREE_NO_INDEX skips it (every kernel
+ * then descends from the deepest common ancestor).  Nothing is built later: renders and
+ * backward calls never allocate or synchronise for it. */
+enum { PO_TREE_NO_INDEX = 1 };
 
 /* Pinhole camera (reading Q5): c2w = camera-to-world 3x4 (OpenGL axes: x right, y up,
  * -z forward; the 3x3 block must be orthonormal within 1e-4), focal lengths and principal
@@ -80,6 +94,8 @@ const char* po_version(void);
  *        fp16 (round to nearest even) when desc->payload == PO_F16.
  * Validates: every index in range and referenced at most once, every node reachable,
  * leaves no deeper than D, finite payload (else PO_ERR_INVALID_TREE).  Synchronous.
+ * Builds the cell index unless desc->flags has PO_TREE_NO_INDEX; PO_ERR_OOM if the index does
+ * not fit (the message names its size; nothing is created then).
  * The caller keeps ownership of the host arrays; *out owns device memory until
  * po_tree_destroy. */
 po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_t n_nodes, const float* sigma,
@@ -115,6 +131,8 @@ po_status po_tree_convert(const po_tree* src, int32_t payload, po_tree** out);
 po_status po_tree_destroy(po_tree* tree);
 /* sh_row_bytes: padded device row of one leaf's SH payload (16-byte multiple). */
 po_status po_tree_info(const po_tree* tree, int64_t* n_nodes, int64_t* n_leaves, int32_t* sh_row_bytes);
+/* Device bytes of the tree's cell index (0 when PO_TREE_NO_INDEX or D outside 2..10). */
+po_status po_tree_index_bytes(const po_tree* tree, int64_t* bytes);
 /* Copy the current leaf values back (host float sigma[n_leaves], sh[n_leaves][B][3]; either may
  * be NULL).  Synchronous (device-wide sync of the tree's device). */
 po_status po_tree_read_leaves(const po_tree* tree, float* sigma, float* sh);
@@ -317,13 +335,20 @@ po_status po_leaf_max_alpha(const po_tree* tree, const float* rays, int64_t n, c
                             float* max_alpha, po_stream stream);
 
 /* ---- parity / measurement helpers ----------------------------------------------------
- * po_trace: the visited-leaf sequence of each ray up to termination (same traversal as
- * po_render_rays).  leaf_ids device int32[n][max_leaves] (first max_leaves, -1 padded;
- * may be NULL when max_leaves == 0), counts device int32[n] (leaves composited, sigma~<=0
- * leaves included, reading Q10), node_counts device int32[n] or NULL (internal nodes,
- * root included, whose box the processed interval meets). */
+ * po_trace: the visited-leaf sequence of each ray up to termination, produced by the very
+ * traversal the product kernels run (po_render, po_render_rays, the backward and the NEXT-row
+ * kernels: the level-(D-1) cell index when the tree has one).  leaf_ids device
+ * int32[n][max_leaves] (first max_leaves, -1 padded; may be NULL when max_leaves == 0), counts
+ * device int32[n] (leaves composited, sigma~<=0 leaves included, reading Q10), node_counts
+ * device int32[n] or NULL (internal nodes, root included, whose box the processed interval
+ * meets: a property of the classic descent, counted by a second launch of it).
+ * flags: 0, or PO_TRACE_CLASSIC = everything from the classic descent from the deepest common
+ * ancestor (the path of trees without an index); both visit the same leaves with the same t
+ * values, which the GPU tests check bit for bit. */
+#define PO_TRACE_CLASSIC 1
 po_status po_trace(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
-                   int32_t max_leaves, int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, po_stream stream);
+                   int32_t max_leaves, int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, int32_t flags,
+                   po_stream stream);
 
 /* po_render_stats: counters of the po_render traversal over n_cams views, ADDED to
  * device uint64 counters[7] = {leaf visits, leaf visits with sigma~ > 0 (SH row read),
@@ -332,7 +357,9 @@ po_status po_trace(const po_tree* tree, const float* rays, int64_t n, const po_r
 po_status po_render_stats(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                           const po_render_opts* opts, unsigned long long* counters, po_stream stream);
 
-/* po_ray_step_timing (measurement, SH-3 fp32 trees): the po_render_rays forward of n rays, one
+/* ---- diagnostics: only in libraries built with -DPO_DIAG (PO_NVCC_EXTRA=-DPO_DIAG); the
+ * symbols exist in every build and return PO_ERR_UNSUPPORTED otherwise ---------------------
+ * po_ray_step_timing (measurement, SH-3 fp32 trees): the po_render_rays forward of n rays, one
  * thread each, recording for every box step k < max_steps of ray i two uint32 at
  * rec[(i * max_steps + k) * 2]: the SM cycles since the previous box step (the previous box's
  * leaf work, the neighbour step and this box's descent) and (child-entry loads of this descent)

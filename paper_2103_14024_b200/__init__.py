@@ -20,11 +20,12 @@ from ._build import LIB as _LIB_PATH
 
 PO_F32, PO_F16 = 0, 1
 PO_SH_CS, PO_SH_NO_CS = 0, 1
+PO_TREE_NO_INDEX = 1
 STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_ERR_OOM", 4: "PO_ERR_CUDA",
           5: "PO_ERR_UNSUPPORTED"}
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
-           "po_tree_info", "po_tree_write_leaves", "po_tree_set_sg_basis", "po_tree_leaf_payload",
+           "po_tree_info", "po_tree_index_bytes", "po_tree_write_leaves", "po_tree_set_sg_basis", "po_tree_leaf_payload",
            "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_render_backward_sgd", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
@@ -40,7 +41,7 @@ class PoError(RuntimeError):
 class TreeDesc(ctypes.Structure):
     _fields_ = [("bbox_min", ctypes.c_float * 3), ("bbox_edge", ctypes.c_float), ("max_depth", ctypes.c_int32),
                 ("sh_degree", ctypes.c_int32), ("payload", ctypes.c_int32), ("sh_sign", ctypes.c_int32),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 class RenderOpts(ctypes.Structure):
@@ -108,7 +109,8 @@ def lib():
         L.po_l2_loss_grad.argtypes = [P, P, I64, P, P, I32, P]
         L.po_tree_sgd_step.argtypes = [P, P, P, F, P]
         L.po_tree_sgd_step_range.argtypes = [P, P, P, F, I64, I64, I32, P]
-        L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, P]
+        L.po_trace.argtypes = [P, P, I64, P, I32, P, P, P, I32, P]
+        L.po_tree_index_bytes.argtypes = [P, P]
         L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_timeline.argtypes = [P, P, I32, I32, I32, P, P, P, P]
         L.po_ray_step_timing.argtypes = [P, P, I64, P, I32, P, P, P]
@@ -185,6 +187,11 @@ class PlenOctree:
         _check(lib().po_tree_info(self.handle, ctypes.byref(nn), ctypes.byref(nl), ctypes.byref(rb)))
         return nn.value, nl.value, rb.value
 
+    def index_bytes(self) -> int:
+        b = ctypes.c_int64()
+        _check(lib().po_tree_index_bytes(self.handle, ctypes.byref(b)))
+        return b.value
+
     def read_leaves(self):
         sig = np.zeros(self.n_leaves, np.float32)
         sh = np.zeros((self.n_leaves, self.B, 3), np.float32)
@@ -239,14 +246,15 @@ class PlenOctree:
 
 
 def po_tree_create(child, sigma, sh, depth: int, sh_degree: int, bbox_min=(-1.0, -1.0, -1.0), edge: float = 2.0,
-                   payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0) -> PlenOctree:
-    """Upload a tree from host arrays (child uint32[n_nodes][8], sigma f32[n_leaves], sh f32[n_leaves][B][3])."""
+                   payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0, index: bool = True) -> PlenOctree:
+    """Upload a tree from host arrays (child uint32[n_nodes][8], sigma f32[n_leaves], sh f32[n_leaves][B][3]);
+    index=False skips the level-(D-1) cell index (PO_TREE_NO_INDEX)."""
     child = np.ascontiguousarray(child, dtype=np.uint32).reshape(-1, 8)
     sigma = np.ascontiguousarray(sigma, dtype=np.float32).reshape(-1)
     B = (sh_degree + 1) ** 2
     sh = np.ascontiguousarray(sh, dtype=np.float32).reshape(sigma.shape[0], B, 3)
     desc = TreeDesc((ctypes.c_float * 3)(*[float(v) for v in bbox_min]), float(edge), int(depth), int(sh_degree),
-                    int(payload), int(sh_sign), int(device))
+                    int(payload), int(sh_sign), int(device), 0 if index else PO_TREE_NO_INDEX)
     h = ctypes.c_void_p()
     _check(lib().po_tree_create(ctypes.byref(desc), _ptr(child), child.shape[0], _ptr(sigma), _ptr(sh),
                                 sigma.shape[0], ctypes.byref(h)))
@@ -262,10 +270,11 @@ def po_tree_convert(tree: PlenOctree, payload: int = PO_F16) -> PlenOctree:
     return PlenOctree(h, desc, tree.n_nodes, tree.n_leaves)
 
 
-def tree_from_gen(tree, payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0) -> PlenOctree:
+def tree_from_gen(tree, payload: int = PO_F32, sh_sign: int = PO_SH_CS, device: int = 0,
+                  index: bool = True) -> PlenOctree:
     """Upload a ``gen.Tree`` (input-generator output)."""
     return po_tree_create(tree.child, tree.sigma, tree.sh, tree.depth, tree.sh_degree, tree.bbox_min, tree.edge,
-                          payload, sh_sign, device)
+                          payload, sh_sign, device, index)
 
 
 def po_render(tree: PlenOctree, cams, W: int, H: int, out=None, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
@@ -491,9 +500,14 @@ def po_tree_sgd_step_range(tree: PlenOctree, grad_sigma, grad_sh, lr: float, beg
                                         PO_SGD_ZERO_GRAD if zero_grad else 0, _stream(stream)))
 
 
+PO_TRACE_CLASSIC = 1
+
+
 def po_trace(tree: PlenOctree, rays, max_leaves: int = 64, gamma: float = 0.01, with_nodes: bool = True,
-             stream=None):
-    """Returns (leaf_ids int32 [n][max_leaves], counts int32 [n], node_counts int32 [n] or None)."""
+             classic: bool = False, stream=None):
+    """Returns (leaf_ids int32 [n][max_leaves], counts int32 [n], node_counts int32 [n] or None).
+    The ids / counts come from the production traversal (cell index), or from the classic descent
+    with classic=True; node counts always from the classic descent."""
     import torch
     rays = _need(rays, torch.float32, (6,))
     n = rays.shape[0]
@@ -503,7 +517,7 @@ def po_trace(tree: PlenOctree, rays, max_leaves: int = 64, gamma: float = 0.01, 
     nodes = torch.empty(n, dtype=torch.int32, device=dev) if with_nodes else None
     o = _opts(gamma, (1.0, 1.0, 1.0))
     _check(lib().po_trace(tree.handle, _ptr(rays), n, ctypes.byref(o), max_leaves, _ptr(ids), _ptr(counts),
-                          _ptr(nodes), _stream(stream)))
+                          _ptr(nodes), PO_TRACE_CLASSIC if classic else 0, _stream(stream)))
     return ids, counts, nodes
 
 

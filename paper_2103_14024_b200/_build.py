@@ -18,8 +18,22 @@ def sources():
                   + glob.glob(os.path.join(PKG, "csrc", "*.h")) + [os.path.join(ROOT, "include", "plenoct.h")])
 
 
+STAMP = LIB + ".flags"   # the extra nvcc flags the library was built with (e.g. -DPO_DIAG)
+PTXAS_INFO = os.path.join(ROOT, "build", "ptxas_info.txt")   # untracked (build/ is git-ignored)
+
+
+def _extra():
+    return os.environ.get("PO_NVCC_EXTRA", "").split()   # -DPO_DIAG: diagnostics build
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read().split() != _extra():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(s) > t for s in sources())
@@ -30,16 +44,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cu = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
     tmp = LIB + f".tmp{os.getpid()}"
-    extra = os.environ.get("PO_NVCC_EXTRA", "").split()   # A/B experiments only (e.g. -DPO_CHILD_LD=1)
+    extra = _extra()
     cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"), *cu, "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+    os.makedirs(os.path.dirname(PTXAS_INFO), exist_ok=True)
+    with open(PTXAS_INFO, "w") as f:
         f.write(res.stderr)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(extra))
     return LIB
 
 

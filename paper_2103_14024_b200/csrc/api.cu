@@ -35,12 +35,11 @@ struct po_tree {
     float* d_img = nullptr;        // scratch image for po_render_host
     size_t img_cap = 0;
     // po_render_host's chunked pipeline (multi-view renders into pinned buffers): two device
-    // chunk buffers, a copy stream and its events, used under pipe_mu
+    // chunk buffers, a copy stream and its events, used under host_mu
     float* d_pipe = nullptr;
     size_t pipe_cap = 0;
     cudaStream_t pipe_stream = nullptr;
     cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // rendered[2], copied[2]
-    std::mutex pipe_mu;
     // po_render_host band pipeline (one view): cumulative per-band tile counters for W x H
     unsigned long long* d_band = nullptr;
     int band_w = 0, band_h = 0;
@@ -52,16 +51,28 @@ struct po_tree {
     unsigned* d_order_zip = nullptr;
     int zip_w = 0, zip_h = 0;
     std::mutex order_mu;
-    // work counters of the persistent render kernel: kWorkSlots pairs, handed out round
-    // robin so up to kWorkSlots renders of one tree may be in flight on different streams
-    static constexpr int kWorkSlots = 64;
+    // work counters of the persistent kernels: one block of kWorkStride words per CUDA stream
+    // that launched on this tree (launches on one stream are serialised, so they may share
+    // a block; the last CTA of each launch resets it).  Up to kWorkSlots distinct streams.
+    static constexpr int kWorkSlots = 256;
+    static constexpr int kWorkStride = 8;
     unsigned* d_work = nullptr;
-    std::atomic<uint32_t> work_rr{0};
-    int next_slot() { return (int)(work_rr.fetch_add(1) % kWorkSlots); }
-    unsigned* work_of(int slot) { return d_work + 2 * slot; }
+    std::mutex work_mu;
+    std::vector<cudaStream_t> work_streams;
+    unsigned* work_for(cudaStream_t s) {
+        std::lock_guard<std::mutex> lk(work_mu);
+        for (size_t i = 0; i < work_streams.size(); ++i)
+            if (work_streams[i] == s) return d_work + kWorkStride * i;
+        if ((int)work_streams.size() >= kWorkSlots) return nullptr;
+        work_streams.push_back(s);
+        return d_work + kWorkStride * (work_streams.size() - 1);
+    }
+    int* sgd_flag() { return reinterpret_cast<int*>(d_work + kWorkStride * kWorkSlots); }
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
-    uint32_t* d_grid = nullptr;      // k_render's dense level-(D-1) cell index (build_grid)
-    bool grid_tried = false;
+    uint32_t* d_grid = nullptr;      // dense level-(D-1) cell index (build_grid, at po_tree_create)
+    size_t grid_bytes = 0;
+    // po_render_host holds this for its whole body (camera / image / pipeline scratch)
+    std::mutex host_mu;
     static constexpr int64_t kPayloadPad = 4096;   // spare zero leaves after the payload arrays
     float4* d_sg = nullptr;          // spherical-Gaussian lobes (po_tree_set_sg_basis) or null
     std::vector<float> h_sg;         // the same on the host, [B][4]
@@ -156,14 +167,16 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
     return d_ord;
 }
 
-// The level-(D-1) cell index of k_render (kOptGrid): for every cell of the 2^(D-1)-per-axis grid
-// the entry of the depth-(D-1) node covering it, a depth-(D-1) leaf's entry, or the level of the
-// empty box containing it (0xFFFFFFFF: a coarser leaf, traversed the classic way).  Built on the
-// host from the caller's child table at the first render of the tree (D in 2..10; 67 MB at
-// D = 9, 537 MB at D = 10), read-only afterwards.  Caller holds order_mu.
-static void build_grid(po_tree* t) {
+// The level-(D-1) cell index (kOptGrid): for every cell of the 2^(D-1)-per-axis grid the entry
+// of the depth-(D-1) node covering it, a depth-(D-1) leaf's entry, or the level of the empty box
+// containing it (0xFFFFFFFF: a coarser leaf, traversed the classic way).  Built on the host from
+// the caller's child table inside po_tree_create (D in 2..10; 67 MB at D = 9, 537 MB at D = 10)
+// unless the descriptor sets PO_TREE_NO_INDEX; read-only afterwards, so renders stay
+// asynchronous and allocation-free.  Returns the CUDA error of the upload (cudaSuccess when D is
+// outside 2..10: every kernel then descends classically).
+static cudaError_t build_grid(po_tree* t) {
     const int D = t->desc.max_depth;
-    if (t->d_grid || D < 1 || D > 10) return;
+    if (t->d_grid || D < 2 || D > 10) return cudaSuccess;
     const int G2 = 1 << (D - 1);
     std::vector<uint32_t> g((size_t)G2 * G2 * G2, 0u);
     auto fill = [&](int x0, int y0, int z0, int n, uint32_t v) {   // grid cells [x0, x0+n)^3
@@ -188,24 +201,21 @@ static void build_grid(po_tree* t) {
             }
         }
     };
-    if (D == 1) return;
     rec(0u, 0, 0, 0, 0);
     uint32_t* d = nullptr;
-    if (cudaMalloc(&d, g.size() * 4) != cudaSuccess) return;
-    if (cudaMemcpy(d, g.data(), g.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaError_t e = cudaMalloc(&d, g.size() * 4);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();   // not sticky: po_tree_create reports it
+        return e;
+    }
+    if ((e = cudaMemcpy(d, g.data(), g.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        (void)cudaGetLastError();
         cudaFree(d);
-        return;
+        return e;
     }
     t->d_grid = d;
-}
-
-// one build attempt per tree; without an index the kernels descend classically
-static void ensure_grid(po_tree* t) {
-    std::lock_guard<std::mutex> lk(t->order_mu);
-    if (!t->grid_tried) {
-        t->grid_tried = true;
-        build_grid(t);
-    }
+    t->grid_bytes = g.size() * 4;
+    return cudaSuccess;
 }
 
 po::DevTree dev_tree(const po_tree* t) {
@@ -269,6 +279,7 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
         return fail(PO_ERR_UNSUPPORTED, "payload %d unsupported", desc->payload);
     if (desc->sh_sign != PO_SH_CS && desc->sh_sign != PO_SH_NO_CS)
         return fail(PO_ERR_INVALID_ARG, "sh_sign %d invalid", desc->sh_sign);
+    if (desc->flags & ~PO_TREE_NO_INDEX) return fail(PO_ERR_INVALID_ARG, "unknown desc flags 0x%x", desc->flags);
     if (n_nodes < 1 || !child) return fail(PO_ERR_INVALID_ARG, "need n_nodes >= 1 and a child table");
     if (n_leaves < 0 || n_leaves > (int64_t)po::kIdxMask + 1 || n_nodes > ((int64_t)1 << 29))
         return fail(PO_ERR_INVALID_ARG, "n_leaves (<= 2^30) / n_nodes (<= 2^29) out of range");
@@ -353,9 +364,10 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
         e = cudaMemset(t->d_sh, 0, (size_t)n_alloc * row * elt);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(sh)"));
     // work counters + one device flag (po_render_backward_sgd: "an overflow ray wrote the buffer")
-    e = cudaMalloc(&t->d_work, sizeof(unsigned) * (2 * po_tree::kWorkSlots + 1));
+    const size_t work_words = (size_t)po_tree::kWorkStride * po_tree::kWorkSlots + 1;
+    e = cudaMalloc(&t->d_work, sizeof(unsigned) * work_words);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "cudaMalloc(work)"));
-    e = cudaMemset(t->d_work, 0, sizeof(unsigned) * (2 * po_tree::kWorkSlots + 1));
+    e = cudaMemset(t->d_work, 0, sizeof(unsigned) * work_words);
     if (e != cudaSuccess) return cleanup(cuda_status(e, "memset(work)"));
     // the device child table is the caller's (ABI encoding, reading Q1)
     e = cudaMemcpy(t->d_child, child, (size_t)n_nodes * 8 * sizeof(uint32_t), cudaMemcpyHostToDevice);
@@ -385,6 +397,13 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
         }
     }
     t->h_child.assign(child, child + (size_t)n_nodes * 8);
+    if (!(desc->flags & PO_TREE_NO_INDEX)) {
+        e = build_grid(t);
+        if (e != cudaSuccess)
+            return cleanup(fail(e == cudaErrorMemoryAllocation ? PO_ERR_OOM : PO_ERR_CUDA,
+                                "level-(D-1) cell index (%.0f MB): %s; PO_TREE_NO_INDEX creates the tree without it",
+                                std::ldexp(1.0, 3 * (D - 1)) * 4 / 1e6, cudaGetErrorString(e)));
+    }
     *out = t;
     return PO_OK;
 }
@@ -517,6 +536,13 @@ po_status po_tree_info(const po_tree* t, int64_t* n_nodes, int64_t* n_leaves, in
     return PO_OK;
 }
 
+po_status po_tree_index_bytes(const po_tree* t, int64_t* bytes) {
+    if (po_status s = check_tree(t)) return s;
+    if (!bytes) return fail(PO_ERR_INVALID_ARG, "bytes is NULL");
+    *bytes = (int64_t)t->grid_bytes;
+    return PO_OK;
+}
+
 po_status po_tree_read_leaves(const po_tree* t, float* sigma, float* sh) {
     if (po_status s = check_tree(t)) return s;
     DeviceGuard g(t->desc.device);
@@ -568,12 +594,12 @@ static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams,
                                   const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
                                   unsigned long long* timeline = nullptr, bool zip = false, bool raster = false) {
     cudaError_t e = cudaSuccess;
-    ensure_grid(t);
     const unsigned* order = raster ? nullptr : block_order(t, W, H, s, &e, zip);
     if (e != cudaSuccess) return cuda_status(e, "block order");
-    const int slot = t->next_slot();
+    unsigned* work = t->work_for(s);
+    if (!work) return fail(PO_ERR_UNSUPPORTED, "%s: more than %d distinct streams on one tree", where, po_tree::kWorkSlots);
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
-                                      out, t->work_of(slot), order, timeline, s),
+                                      out, work, order, timeline, s),
                     where);
 }
 
@@ -622,6 +648,9 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
     if (po_status s = check_cams_host(cams_host, n_cams)) return s;
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    // one host render per tree at a time: the camera, image and pipeline scratch are per tree
+    // (the call synchronises its stream before returning, so this costs no overlap)
+    std::lock_guard<std::mutex> host_lk(t->host_mu);
     cudaStream_t s = (cudaStream_t)stream;
     if (t->cam_cap < n_cams) {
         if (t->d_cams) cudaFree(t->d_cams);
@@ -665,7 +694,6 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
         return !(ev && std::strcmp(ev, "0") == 0);
     }();
     if (direct && pipe_ok && n_cams >= 4 && out_bytes > ((size_t)12 << 20)) {
-        std::lock_guard<std::mutex> lk(t->pipe_mu);
         const int chunk = n_cams >= 32 ? 16 : (n_cams + 1) / 2;   // views per render launch
         const size_t view_floats = (size_t)W * H * 3;
         const size_t cfloats = (size_t)chunk * view_floats;
@@ -740,7 +768,6 @@ po_status po_render_host(const po_tree* tc, const po_camera* cams_host, int32_t 
     // bands (the costly centre rows finish last) would be copied after the kernel -- in-kernel
     // stores win there (c1 800x800: 3700 vs 2545 FPS end to end; c3 1920x1080: 1878 vs 1126).
     if (direct && n_cams == 1 && wait64 != nullptr && out_bytes > ((size_t)12 << 20)) {
-        std::lock_guard<std::mutex> lk(t->pipe_mu);
         const int by_n = (H + 15) / 16, bx_n = (W + 15) / 16;
         const int band_rows = (by_n + 7) / 8;   // 8 bands
         const int nb = (by_n + band_rows - 1) / band_rows;
@@ -882,11 +909,11 @@ po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const p
     if (!rays || !out_rgb) return fail(PO_ERR_INVALID_ARG, "rays / out_rgb NULL");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    po_tree* tm = const_cast<po_tree*>(t);   // only the work counters and the cell index are mutated
-    ensure_grid(tm);
+    po_tree* tm = const_cast<po_tree*>(t);   // only the work counters are mutated
+    unsigned* work = tm->work_for((cudaStream_t)stream);
+    if (!work) return fail(PO_ERR_UNSUPPORTED, "more than %d distinct streams on one tree", po_tree::kWorkSlots);
     return launched(po::launch_render_rays(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, o,
-                                           out_rgb, aux, leaf_span, sg, (cudaStream_t)stream,
-                                           tm->work_of(tm->next_slot())),
+                                           out_rgb, aux, leaf_span, sg, (cudaStream_t)stream, work),
                     "po_render_rays");
 }
 
@@ -933,8 +960,6 @@ po_status po_backward_plan(po_tree* t, const uint32_t* leaf_span, int64_t n, int
     std::lock_guard<std::mutex> lk(t->plan_mu);
     if (t->plan_cap < need) {
         if (t->d_plan) cudaFree(t->d_plan);
-    if (t->d_det) cudaFree(t->d_det);
-    if (t->d_sg) cudaFree(t->d_sg);
         t->d_plan = nullptr;
         t->plan_cap = 0;
         e = cudaMalloc(&t->d_plan, need);
@@ -970,12 +995,13 @@ po_status po_render_backward_chunk(const po_tree* t, const float* rays, const in
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     po_tree* mt = const_cast<po_tree*>(t);   // work counters only
+    unsigned* work = mt->work_for((cudaStream_t)stream);
+    if (!work) return fail(PO_ERR_UNSUPPORTED, "more than %d distinct streams on one tree", po_tree::kWorkSlots);
     if (segments != nullptr && aux != nullptr) g_launches.fetch_add(1);   // + the replay kernel
     return launched(po::launch_backward_chunk(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, perm,
                                               chunk_ray_end, chunk, dL_dC, aux, sg, o, grad_sigma, grad_sh,
-                                              mt->work_of(mt->next_slot()), (cudaStream_t)stream),
+                                              work, (cudaStream_t)stream),
                     "po_render_backward_chunk");
 }
 
@@ -993,7 +1019,6 @@ po_status po_render_backward(const po_tree* t, const float* rays, int64_t n, con
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     if (segments != nullptr && aux != nullptr) g_launches.fetch_add(1);   // replay + overflow re-traversal
     return launched(po::launch_backward(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, rays, n, dL_dC, aux,
                                         sg, o, grad_sigma, grad_sh, (cudaStream_t)stream),
@@ -1017,11 +1042,10 @@ po_status po_render_backward_sgd(po_tree* t, const float* rays, int64_t n, const
     if (((uintptr_t)grad_sh & 15u) != 0) return fail(PO_ERR_INVALID_ARG, "grad_sh must be 16-byte aligned");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     g_launches.fetch_add(2);   // overflow re-traversal + fused replay + gated SGD
     return launched(po::launch_backward_sgd(dev_tree(t), t->desc.sh_degree, rays, n, dL_dC, aux, sg, o, t->d_sigma,
                                             static_cast<float*>(t->d_sh), t->sh_row, t->n_leaves, lr, grad_sigma,
-                                            grad_sh, reinterpret_cast<int*>(t->d_work + 2 * po_tree::kWorkSlots),
+                                            grad_sh, t->sgd_flag(),
                                             (cudaStream_t)stream),
                     "po_render_backward_sgd");
 }
@@ -1053,7 +1077,6 @@ po_status po_render_backward_deterministic(const po_tree* tc, const float* rays,
         return fail(PO_ERR_UNSUPPORTED, "n * max_seg >= 2^31 (32-bit segment slots)");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    ensure_grid(t);   // the cell index the overflow re-traversal reads
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     if (n_overflow && (e = cudaMemsetAsync(n_overflow, 0, sizeof(int32_t), s)) != cudaSuccess)
@@ -1160,17 +1183,18 @@ po_status po_tree_sgd_step(po_tree* t, const float* grad_sigma, const float* gra
 }
 
 po_status po_trace(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, int32_t max_leaves,
-                   int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, po_stream stream) {
+                   int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, int32_t flags, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
     po::RenderOpts o;
     if (po_status s = check_opts(opts, &o)) return s;
     if (n < 0 || max_leaves < 0) return fail(PO_ERR_INVALID_ARG, "n < 0 or max_leaves < 0");
     if (n == 0) return PO_OK;
     if (!rays || (max_leaves > 0 && !leaf_ids)) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
+    if (flags & ~PO_TRACE_CLASSIC) return fail(PO_ERR_INVALID_ARG, "unknown flags %d", flags);
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_trace(dev_tree(t), rays, n, o.gamma, max_leaves, max_leaves > 0 ? leaf_ids : nullptr,
-                                     counts, node_counts, (cudaStream_t)stream),
+                                     counts, node_counts, (flags & PO_TRACE_CLASSIC) != 0, (cudaStream_t)stream),
                     "po_trace");
 }
 
@@ -1184,7 +1208,6 @@ po_status po_render_depth(const po_tree* t, const float* rays, int64_t n, const 
     if (!rays || !alpha || !depth) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     return launched(po::launch_render_depth(dev_tree(t), rays, n, o.gamma, alpha, depth, (cudaStream_t)stream),
                     "po_render_depth");
 }
@@ -1199,7 +1222,6 @@ po_status po_leaf_max_alpha(const po_tree* t, const float* rays, int64_t n, cons
     if (!rays || !max_alpha) return fail(PO_ERR_INVALID_ARG, "NULL buffer");
     DeviceGuard g(t->desc.device);
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
-    ensure_grid(const_cast<po_tree*>(t));   // the cell index the traversal kernels read
     return launched(po::launch_leaf_max_alpha(dev_tree(t), rays, n, o.gamma, max_alpha, (cudaStream_t)stream),
                     "po_leaf_max_alpha");
 }
@@ -1207,6 +1229,9 @@ po_status po_leaf_max_alpha(const po_tree* t, const float* rays, int64_t n, cons
 po_status po_render_timeline(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                              const po_render_opts* opts, float* out_rgb, unsigned long long* timeline,
                              po_stream stream) {
+#ifndef PO_DIAG
+    return fail(PO_ERR_UNSUPPORTED, "%s: diagnostics are built only with -DPO_DIAG", "po_render_timeline");
+#else
     if (po_status s = check_tree(t)) return s;
     if (po_status s = check_image(n_cams, W, H)) return s;
     po::RenderOpts o;
@@ -1217,10 +1242,14 @@ po_status po_render_timeline(const po_tree* t, const po_camera* cams, int32_t n_
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return render_scheduled(const_cast<po_tree*>(t), cams, n_cams, W, H, o, out_rgb, (cudaStream_t)stream,
                             "po_render_timeline", timeline);
+#endif
 }
 
 po_status po_ray_step_timing(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts,
                              int32_t max_steps, uint32_t* rec, int32_t* steps, po_stream stream) {
+#ifndef PO_DIAG
+    return fail(PO_ERR_UNSUPPORTED, "%s: diagnostics are built only with -DPO_DIAG", "po_ray_step_timing");
+#else
     if (po_status s = check_tree(t)) return s;
     po::RenderOpts o;
     if (po_status s = check_opts(opts, &o)) return s;
@@ -1233,6 +1262,7 @@ po_status po_ray_step_timing(const po_tree* t, const float* rays, int64_t n, con
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return launched(po::launch_ray_step_timing(dev_tree(t), rays, n, o, max_steps, rec, steps, (cudaStream_t)stream),
                     "po_ray_step_timing");
+#endif
 }
 
 po_status po_render_stats(const po_tree* t, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,

@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             }
             RayState r;
             if (ray_setup(tr, o, d, r)) {
+#ifdef PO_DIAG
                 if constexpr ((OPT & kOptProbeNoShade) != 0) {
                     // measurement probe only (PO_RENDER_OPT=64, wrong colours): the traversal and
                     // transmittance without any SH row, to size a traversal/shading split
@@ -418,7 +419,9 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                     } v{tr, 1.f, opt.gamma};
                     traverse<kOptLean>(tr, r, v, stk);
                     C[0] = C[1] = C[2] = v.T;
-                } else {
+                } else
+#endif
+                {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
                     traverse<OPT & (kOptLean | kOptGrid)>(tr, r, v, stk);
 #pragma unroll
@@ -552,6 +555,7 @@ __global__ void __launch_bounds__(256, 2) k_render_rays_p(DevTree tr, const floa
     }
 }
 
+#ifdef PO_DIAG
 // Measurement variants of the plain forward over a ray list (PO_RAYS_OPT, SH-3 fp32 only):
 // 128 = the default lean step, 64 = traversal + T only (wrong colours).  Used by
 // tools/diag_tail.py to time single warp tiles alone ("where the tail comes from").
@@ -657,6 +661,8 @@ cudaError_t launch_ray_step_timing(const DevTree& tr, const float* rays, int64_t
     k_ray_step_timing<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tr, rays, n, opt, max_steps, rec, steps);
     return cudaGetLastError();
 }
+
+#endif  // PO_DIAG
 
 struct SegIn {
     const float4* __restrict__ rec;
@@ -1090,6 +1096,10 @@ __global__ void __launch_bounds__(256) k_leaf_max_alpha(DevTree tr, const float*
     if (ray_setup(tr, o, d, r)) traverse<kOptDefault | kOptGrid>(tr, r, v, stk);
 }
 
+// Parity / measurement trace.  GRID = the production traversal (the level-(D-1) cell index when
+// the tree has one, exactly as k_render / k_render_rays / the backward run it); !GRID = the
+// classic descent from the deepest common ancestor, which also counts the internal nodes met.
+template <bool GRID>
 __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restrict__ rays, int64_t n, float gamma,
                                                int32_t max_leaves, int32_t* __restrict__ leaf_ids,
                                                int32_t* __restrict__ counts, int32_t* __restrict__ node_counts) {
@@ -1106,7 +1116,10 @@ __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restri
     for (int j = 0; j < max_leaves && ids; ++j) ids[j] = -1;
     TraceVisitor v{tr, 1.f, gamma, ids, ids ? max_leaves : 0, 0, 0};
     RayState r;
-    if (ray_setup(tr, o, d, r)) traverse(tr, r, v, stk);
+    if (ray_setup(tr, o, d, r)) {
+        if constexpr (GRID) traverse<kOptDefault | kOptGrid>(tr, r, v, stk);
+        else traverse<kOptDefault>(tr, r, v, stk);
+    }
     if (counts) counts[i] = v.count;
     if (node_counts) node_counts[i] = v.nodes;
 }
@@ -1304,11 +1317,15 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     // Rule in warp tiles per SM: < 200 -> 2, < 4000 -> 3, else 4.  PO_RENDER_MINB=1..4
     // overrides it; PO_RENDER_OPT (0 = plain neighbour step, 64 = traversal-only probe;
     // traverse.cuh) selects SH-3 fp32 variants for A/B experiments.
+#ifdef PO_DIAG
     static const int env_minb = [] {
         const char* e = getenv("PO_RENDER_MINB");
         const int v = e ? atoi(e) : 0;
         return (v >= 1 && v <= 4) ? v : 0;
     }();
+#else
+    constexpr int env_minb = 0;
+#endif
     static const int n_sm = [] {
         int dev = 0, v = 148;
         if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
@@ -1317,11 +1334,15 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
     }();
     const int64_t tiles_per_sm = tiles / n_sm;
     const int minb = env_minb ? env_minb : (tiles_per_sm < 200 ? 2 : (tiles_per_sm < 4000 ? 3 : 4));
+#ifdef PO_DIAG
     static const int vopt = [] {
         const char* e = getenv("PO_RENDER_OPT");
         const int v = e ? atoi(e) : kRenderOptDefault;
         return (v == kOptPlain || v == kOptProbeNoShade || v == kOptLean) ? v : kRenderOptDefault;
     }();
+#else
+    constexpr int vopt = kRenderOptDefault;
+#endif
     using KFn = void (*)(DevTree, const po_camera*, int, int, int, RenderOpts, float*, unsigned*, const unsigned*,
                          unsigned long long*);
     KFn fn = nullptr;
@@ -1331,13 +1352,17 @@ cudaError_t launch_render(const DevTree& tr, int deg, bool f16, const po_camera*
         static const KFn k16[4] = {k_render<3, true, 1, kRenderOptDefault>, k_render<3, true, 2, kRenderOptDefault>,
                                    k_render<3, true, 3, kRenderOptDefault>, k_render<3, true, 4, kRenderOptDefault>};
         fn = f16 ? k16[minb - 1] : k32[minb - 1];
-    } else if (deg == 3 && !f16) {
+    }
+#ifdef PO_DIAG
+    else if (deg == 3 && !f16) {
         static const KFn probe[4] = {k_render<3, false, 1, kOptProbeNoShade>, k_render<3, false, 2, kOptProbeNoShade>,
                                      k_render<3, false, 3, kOptProbeNoShade>, k_render<3, false, 4, kOptProbeNoShade>};
         if (vopt == kOptProbeNoShade) fn = probe[minb - 1];
         else if (vopt == kOptLean) fn = k_render<3, false, 2, kOptLean>;   // without the index
         else fn = k_render<3, false, 2, kOptPlain>;
-    } else {
+    }
+#endif
+    else {
         PO_DISPATCH(deg, f16, fn = k_render<DEG, F16, 2, kRenderOptDefault>);
     }
     const size_t dyn = 0;
@@ -1360,6 +1385,7 @@ cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float
                                cudaStream_t s, unsigned* work) {
     if (n == 0) return cudaSuccess;
     const SegOut so{static_cast<float4*>(sg.rec), sg.count, sg.n, sg.max_seg};
+#ifdef PO_DIAG
     static const int dopt = [] {   // measurement variants (k_render_rays_diag)
         const char* e = getenv("PO_RAYS_OPT");
         return e ? atoi(e) : 0;
@@ -1375,6 +1401,9 @@ cudaError_t launch_render_rays(const DevTree& tr, int deg, bool f16, const float
         const char* e = getenv("PO_RAYS_PERSIST");
         return !(e && std::strcmp(e, "0") == 0);
     }();
+#else
+    constexpr bool persist = true;
+#endif
     if (persist && work != nullptr && (n + 31) / 32 < (int64_t)0xFFFFFFF0u) {
         PO_DISPATCH(deg, f16, {
             static const int grid = persistent_grid(k_render_rays_p<DEG, F16>, 1 << 30, 0);
@@ -1496,10 +1525,19 @@ cudaError_t launch_leaf_max_alpha(const DevTree& tr, const float* rays, int64_t 
 }
 
 cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
-                         int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s) {
+                         int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, bool classic, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    carveout_once(k_trace);
-    k_trace<<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, max_leaves, leaf_ids, counts, node_counts);
+    if (classic || tr.grid == nullptr) {
+        carveout_once(k_trace<false>);
+        k_trace<false><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, max_leaves, leaf_ids, counts, node_counts);
+        return cudaGetLastError();
+    }
+    carveout_once(k_trace<true>);
+    k_trace<true><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, max_leaves, leaf_ids, counts, nullptr);
+    if (node_counts != nullptr) {   // the node count is a property of the classic descent
+        carveout_once(k_trace<false>);
+        k_trace<false><<<grid1d(n, 256), 256, 0, s>>>(tr, rays, n, gamma, 0, nullptr, nullptr, node_counts);
+    }
     return cudaGetLastError();
 }
 

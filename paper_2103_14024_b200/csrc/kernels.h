@@ -81,7 +81,7 @@ cudaError_t launch_render_depth(const DevTree& tr, const float* rays, int64_t n,
 cudaError_t launch_leaf_max_alpha(const DevTree& tr, const float* rays, int64_t n, float gamma, float* max_alpha,
                                   cudaStream_t s);
 cudaError_t launch_trace(const DevTree& tr, const float* rays, int64_t n, float gamma, int32_t max_leaves,
-                         int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, cudaStream_t s);
+                         int32_t* leaf_ids, int32_t* counts, int32_t* node_counts, bool classic, cudaStream_t s);
 cudaError_t launch_stats(const DevTree& tr, const po_camera* cams, int n_cams, int W, int H, float gamma,
                          unsigned long long* counters, cudaStream_t s);
 cudaError_t launch_l2_loss(const float* pred, const float* target, int64_t n3, float* dL_dC, double* loss,

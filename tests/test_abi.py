@@ -38,16 +38,16 @@ def test_product_does_not_import_oracle():
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).lower().replace("no cpu", ""), f
 
 
-def _desc(po, depth=2, deg=0, payload=0):
-    return po.TreeDesc((ctypes.c_float * 3)(-1, -1, -1), 2.0, depth, deg, payload, 0, 0)
+def _desc(po, depth=2, deg=0, payload=0, flags=0):
+    return po.TreeDesc((ctypes.c_float * 3)(-1, -1, -1), 2.0, depth, deg, payload, 0, 0, flags)
 
 
-def _create(po, child, sigma, sh, depth=2, deg=0, payload=0):
+def _create(po, child, sigma, sh, depth=2, deg=0, payload=0, flags=0):
     child = np.ascontiguousarray(child, np.uint32)
     sigma = np.ascontiguousarray(sigma, np.float32)
     sh = np.ascontiguousarray(sh, np.float32)
     h = ctypes.c_void_p()
-    d = _desc(po, depth, deg, payload)
+    d = _desc(po, depth, deg, payload, flags)
     st = po.lib().po_tree_create(ctypes.byref(d), child.ctypes.data, child.shape[0], sigma.ctypes.data,
                                  sh.ctypes.data, sigma.shape[0], ctypes.byref(h))
     return st, po.lib().po_last_error().decode()
@@ -79,6 +79,9 @@ def test_rejects_malformed_trees(po):
     assert st == 5
     st, _ = _create(po, [[0] * 8], [], np.zeros((0, 1, 3)), depth=0)
     assert st == 1
+    # unknown descriptor flags
+    st, msg = _create(po, [[0] * 8], [], np.zeros((0, 1, 3)), depth=1, flags=4)
+    assert st == 1 and "flags" in msg
 
 
 def test_rejects_bad_args_without_gpu(po):
@@ -99,7 +102,11 @@ def test_rejects_bad_args_without_gpu(po):
     h = ctypes.c_void_p()
     assert L.po_tree_convert(None, 1, ctypes.byref(h)) == 1 and h.value is None
     assert L.po_tree_sgd_step_range(None, None, None, ctypes.c_float(1.0), 0, 1, 0, None) == 1
-    assert L.po_ray_step_timing(None, None, 1, ctypes.byref(o), 8, None, None, None) == 1
+    # diagnostics exist in every build and are refused unless built with -DPO_DIAG
+    assert L.po_ray_step_timing(None, None, 1, ctypes.byref(o), 8, None, None, None) == 5
+    assert L.po_render_timeline(None, None, 1, 8, 8, ctypes.byref(o), None, None, None) == 5
+    assert L.po_trace(None, None, 1, ctypes.byref(o), 0, None, None, None, 0, None) == 1
+    assert L.po_tree_index_bytes(None, None) == 1
     assert L.po_render_backward_sgd(None, None, 1, None, None, None, ctypes.byref(o), ctypes.c_float(1.0), None, None,
                                     None) == 1
 
