@@ -54,7 +54,7 @@ def lib():
         _lib.or_trace_ray.restype = I64
         _lib.or_render.argtypes = [P, P, I64, D, P, ctypes.c_int, P, P, P, I32, P, P, ctypes.c_int]
         _lib.or_backward.argtypes = [P, P, I64, D, P, P, P, P, ctypes.c_int, P, P]
-        _lib.or_tie_flags.argtypes = [P, P, I64, D, D, D, P, ctypes.c_int]
+        _lib.or_tie_flags.argtypes = [P, P, I64, D, D, P, P, ctypes.c_int]
         _lib.or_render_depth.argtypes = [P, P, I64, D, P, P, ctypes.c_int]
         _lib.or_leaf_max_alpha.argtypes = [P, P, I64, D, P, ctypes.c_int]
         _lib.or_sg_basis.argtypes = [ctypes.c_int, P, P, I64, P, P]
@@ -189,14 +189,16 @@ def backward(ot: OracleTree, rays, dL_dC, gamma: float = 0.0, bg=(1.0, 1.0, 1.0)
     return (gs, gk, ss, sk) if with_scale else (gs, gk)
 
 
-def tie_flags(ot: OracleTree, rays, gamma: float = 0.01, tol_plane: float = 1e-6, tol_gamma: float = 2e-2,
-              nthreads: int = 0) -> np.ndarray:
-    """Tie tags of DESIGN.md reading Q27.  tol_gamma = 2e-2 (not the survey's 1e-4): an fp32 ray
-    (origin, direction rounded to fp32, crossings at t ~ 3-4) carries segment-length errors
-    e_delta ~ 1e-6 world units, so with sigma up to 768 (c1, sigma_max h = 3) and up to ~15
-    segments before termination T is only known to ~ sigma_max * N * e_delta ~ 1e-2 relative;
-    rays whose T passes within that band of gamma can legitimately stop one segment apart."""
+def tie_flags(ot: OracleTree, rays, gamma: float = 0.01, eps: float = 2.0 ** -24, nthreads: int = 0,
+              with_bound: bool = False):
+    """Tie tags of reading Q27 for an implementation with unit roundoff eps (fp32 by
+    default): bit0 an undetermined order of two plane crossings where a leaf touches them, bit1 a
+    processed segment within the error of its ends, bit2 T within its error band of gamma before
+    the stop, bit3 the origin on a level-D plane.  Every bound is the fp32 error of the crossing
+    t = (p - o)/d, evaluated per crossing (plenoct_oracle.cpp, or_tie_flags).  with_bound also
+    returns, per ray, the bound on |C_impl - C_oracle| those ties allow (0 for tie-free rays)."""
     rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
     f = np.zeros(rays.shape[0], np.uint8)
-    lib().or_tie_flags(ot.ref, _ptr(rays), rays.shape[0], gamma, tol_plane, tol_gamma, _ptr(f), nthreads)
-    return f
+    b = np.zeros(rays.shape[0]) if with_bound else None
+    lib().or_tie_flags(ot.ref, _ptr(rays), rays.shape[0], gamma, eps, _ptr(f), _ptr(b), nthreads)
+    return (f, b) if with_bound else f

@@ -612,19 +612,64 @@ int or_leaf_max_alpha(const or_tree* T, const double* rays, int64_t n, double ga
     return 0;
 }
 
-// Tie tags (reading Q27).  bit0: two level-D plane crossings (or t_near / t_far) inside
-// [t_near, t_far] closer than tol_plane*edge; bit1: a processed delta < tol_plane*edge;
-// bit2: some T_{i+1} within tol_gamma*gamma of gamma; bit3: origin inside the box within
-// tol_plane*edge of a level-D plane.
-int or_tie_flags(const or_tree* T, const double* rays, int64_t n, double gamma, double tol_plane, double tol_gamma,
-                 uint8_t* flags, int nthreads) {
+// Tie tags (reading Q27).  A ray is a tie when an implementation that evaluates the
+// same definition in floating point with unit roundoff `eps` (2^-24 for fp32) may legitimately
+// produce a different visited-leaf sequence or stop at a different segment.  Such an
+// implementation computes a plane crossing t = (p - o_k)/d_k with an absolute error of at most
+//   e(t) = 2 eps |o_k - b_k| / |d_k| + 12 eps t      (world units; o rounded into grid units,
+//                                                    one subtraction, one reciprocal, products)
+// -- the oracle evaluates the bound in double for every crossing it uses.
+//   bit0: two consecutive crossings (level-D planes on any axis, t_near, t_far) inside
+//         [t_near, t_far], up to the stop, whose order is not determined (gap <= e_a + e_b),
+//         where a LEAF touches the crossing point (probes straddling both planes): only then can
+//         a different order change the visited leaves;
+//   bit1: a processed segment no longer than the error of its two ends;
+//   bit2: some T_{i+1} within its error band of gamma up to the stop;
+//   bit3: the origin (inside the box) within its rounding error of a level-D plane.
+// The band is the optical-depth error sum_k sigma_k (e(t_in,k) + e(t_out,k)) + 10 eps per
+// segment, plus 2 (e_a + e_b) sigma_max for every bit-0 crossing pair (a sliver leaf that may be
+// entered or skipped).  C = sum_i T_i alpha_i c_i + T_N c_N with colours in [0, 1] moves by at
+// most |d tau| when one segment's optical depth tau moves by d tau, so
+//   bound = band + [bit2] gamma (1 + band)
+// bounds |C_impl - C_oracle| of the ray beyond the implementation's own rounding (optional
+// output; the GPU tests assert it on every excluded ray).
+namespace {
+struct Crossing {
+    double t, e;
+};
+
+// entry of the tree at point q (0 = empty / outside): plain walk down the child table
+uint32_t entry_at(const or_tree* T, const double q[3]) {
+    double u[3];
+    for (int k = 0; k < 3; ++k) {
+        u[k] = (q[k] - T->bbox_min[k]) / T->edge;
+        if (!(u[k] >= 0.0 && u[k] < 1.0)) return 0u;
+    }
+    int64_t node = 0;
+    for (int level = 0; level < 62; ++level) {
+        double n = std::ldexp(1.0, level + 1);
+        int oct = 0;
+        for (int k = 0; k < 3; ++k) oct |= (int)((int64_t)std::floor(u[k] * n) & 1) << (2 - k);
+        uint32_t e = T->child[node * 8 + oct];
+        if ((e >> 30) != 1u) return e;
+        node = e & 0x3FFFFFFFu;
+    }
+    return 0u;
+}
+}  // namespace
+
+int or_tie_flags(const or_tree* T, const double* rays, int64_t n, double gamma, double eps, uint8_t* flags,
+                 double* bound, int nthreads) {
     int nt = set_threads(nthreads);
-    double tol = tol_plane * T->edge;
     int64_t G = (int64_t)1 << T->depth;
 #pragma omp parallel num_threads(nt)
     {
         Ctx cx;
-        std::vector<double> ts;
+        std::vector<Crossing> cs;
+        struct Tie {
+            double t, dtau;
+        };
+        std::vector<Tie> ties;
 #pragma omp for schedule(dynamic, 64)
         for (int64_t i = 0; i < n; ++i) {
             Ray r = make_ray(rays + i * 6);
@@ -632,37 +677,91 @@ int or_tie_flags(const or_tree* T, const double* rays, int64_t n, double gamma, 
             bool hit;
             segments(T, r, 0, nullptr, cx, &tn, &tf, &hit);
             uint8_t f = 0;
+            double bnd = 0.0;
             if (hit) {
-                ts.clear();
-                ts.push_back(tn);
-                ts.push_back(tf);
+                double slope[3];   // |o_k - b_k| / |d_k|: the crossing error per axis
+                for (int k = 0; k < 3; ++k)
+                    slope[k] = r.d[k] != 0.0 ? std::fabs(r.o[k] - T->bbox_min[k]) / std::fabs(r.d[k]) : 0.0;
+                auto err = [&](int k, double t) { return 2.0 * eps * slope[k] + 12.0 * eps * t; };
+                cs.clear();
+                double e_tn = 0.0, e_tf = 0.0;   // t_near / t_far: the bbox face that sets them
                 for (int k = 0; k < 3; ++k) {
                     if (r.d[k] == 0.0) continue;
                     for (int64_t j = 0; j <= G; ++j) {
                         double plane = T->bbox_min[k] + T->edge * ((double)j / (double)G);
                         double t = (plane - r.o[k]) / r.d[k];
-                        if (t > tn && t < tf) ts.push_back(t);
+                        if (t == tn && tn > 0.0) e_tn = std::max(e_tn, err(k, t));
+                        if (t == tf) e_tf = std::max(e_tf, err(k, t));
+                        if (t > tn && t < tf) cs.push_back({t, err(k, t)});
                     }
                 }
-                std::sort(ts.begin(), ts.end());
-                for (size_t a = 1; a < ts.size(); ++a)
-                    if (ts[a] - ts[a - 1] < tol) f |= 1;
-                double Tr = 1.0;
+                cs.push_back({tn, e_tn});
+                cs.push_back({tf, e_tf});
+                std::sort(cs.begin(), cs.end(), [](const Crossing& a, const Crossing& b) { return a.t < b.t; });
+                auto e_of = [&](double t) {   // error of a segment end: the crossing with that exact t
+                    auto it = std::lower_bound(cs.begin(), cs.end(), t,
+                                               [](const Crossing& a, double v) { return a.t < v; });
+                    double e = 0.0;
+                    for (; it != cs.end() && it->t == t; ++it) e = std::max(e, it->e);
+                    return e;
+                };
+                // undetermined crossing orders where a leaf touches the crossing point
+                ties.clear();
+                for (size_t a = 1; a < cs.size(); ++a) {
+                    const Crossing& p = cs[a - 1];
+                    const Crossing& q = cs[a];
+                    double tol = p.e + q.e;
+                    if (q.t - p.t > tol) continue;
+                    double tm = 0.5 * (p.t + q.t), h = 3.0 * tol + 1e-12 * T->edge;
+                    bool leaf = false;
+                    double smax = 0.0;
+                    for (int c = 0; c < 8; ++c) {
+                        double pt[3];
+                        for (int k = 0; k < 3; ++k) pt[k] = r.o[k] + tm * r.d[k] + (((c >> k) & 1) ? h : -h);
+                        uint32_t e = entry_at(T, pt);
+                        if ((e >> 30) == 2u) {
+                            leaf = true;
+                            smax = std::max(smax, (double)T->sigma[e & 0x3FFFFFFFu]);
+                        }
+                    }
+                    if (leaf) ties.push_back({tm, 2.0 * tol * smax});
+                }
+                // forward up to the stop: bits 1 and 2, the band, and the stop itself
+                double Tr = 1.0, band = 0.0, t_stop = tf;
+                size_t ti = 0;
+                bool near_gamma = false;
                 for (const Seg& s : cx.segs) {
-                    if (s.t1 - s.t0 < tol) f |= 2;
+                    double ea = e_of(s.t0), eb = e_of(s.t1);
+                    if (s.t1 - s.t0 <= ea + eb) f |= 2;
                     double sig = std::max((double)T->sigma[s.leaf], 0.0);
                     Tr *= std::exp(-sig * (s.t1 - s.t0));
-                    if (gamma > 0 && std::fabs(Tr - gamma) < tol_gamma * gamma) f |= 4;
-                    if (Tr < gamma) break;
+                    band += sig * (ea + eb) + 10.0 * eps;
+                    for (; ti < ties.size() && ties[ti].t <= s.t1 + eb; ++ti) {
+                        band += ties[ti].dtau;
+                        f |= 1;
+                    }
+                    if (gamma > 0 && std::fabs(Tr - gamma) <= band * std::max(Tr, gamma)) near_gamma = true;
+                    if (Tr < gamma) {
+                        t_stop = s.t1 + eb;
+                        break;
+                    }
                 }
+                for (; ti < ties.size() && ties[ti].t <= t_stop; ++ti) {   // ties after the last segment
+                    band += ties[ti].dtau;
+                    f |= 1;
+                }
+                if (near_gamma) f |= 4;
+                bnd = band + (near_gamma ? gamma * (1.0 + band) : 0.0);
                 if (tn == 0.0) {
                     for (int k = 0; k < 3; ++k) {
                         double u = (r.o[k] - T->bbox_min[k]) / T->edge * (double)G;
-                        if (std::fabs(u - std::round(u)) * T->edge / (double)G < tol) f |= 8;
+                        double dist = std::fabs(u - std::round(u)) * T->edge / (double)G;
+                        if (dist <= 4.0 * eps * (std::fabs(r.o[k] - T->bbox_min[k]) + T->edge)) f |= 8;
                     }
                 }
             }
             flags[i] = f;
+            if (bound) bound[i] = bnd;
         }
     }
     return 0;

@@ -80,24 +80,33 @@ def test_leaf_max_alpha_matches_oracle(env, name, gamma):
 
 
 def test_c1_depth_and_filter_sampled(env, c1_tree):
-    """c1 scale: 20,000 random pixels of view 0 (tie-free), depth/alpha and the filter
-    statistic of the leaves they reach."""
+    """c1 scale: 20,000 random pixels of view 0 (tie-free, >= 95 %), depth/alpha and the filter
+    statistic of the leaves they reach.  Bars: 1e-4 plus the ray's optical-depth error band
+    (reading Q27: with sigma up to 768 the fp32 crossings move a segment's optical depth by
+    sigma * (e_in + e_out); alpha = 1 - T moves by at most that sum, the expected depth by at
+    most t_far times twice it, a leaf's max alpha by at most the largest band of its rays)."""
     po, om, torch = env
     cam, W, H = gen.config_camera("c1", 0)
     g = np.random.default_rng(5)
     pix = g.choice(W * H, 20000, replace=False)
-    rays = om.camera_rays(cam, W, H)[pix]
+    rays = om.camera_rays(cam, W, H)[pix].astype(np.float32).astype(np.float64)
     ot = om.OracleTree(c1_tree)
-    rays = rays[_tie_free(om, ot, rays, 0.01)].astype(np.float32)
+    f, band = om.tie_flags(ot, rays, gamma=0.01, with_bound=True)
+    ok = f == 0
+    assert ok.mean() >= 0.95
+    rays, band = rays[ok], band[ok]
     tree = po.tree_from_gen(c1_tree)
-    r = torch.from_numpy(rays).cuda()
+    r = torch.from_numpy(rays.astype(np.float32)).cuda()
     a, d = po.po_render_depth(tree, r, gamma=0.01)
-    ra, rd = om.render_depth(ot, rays.astype(np.float64), gamma=0.01)
-    assert np.abs(a.cpu().numpy() - ra).max() <= 2e-3   # c1 sigma up to 768 (reading Q26)
-    assert (np.abs(d.cpu().numpy() - rd) / np.maximum(1.0, np.abs(rd))).max() <= 2e-3
+    ra, rd = om.render_depth(ot, rays, gamma=0.01)
+    assert np.all(np.abs(a.cpu().numpy() - ra) <= TOL + band)
+    t_far = np.linalg.norm(rays[:, :3], axis=1) + 2.0 * np.sqrt(3.0)   # beyond any exit of [-1,1]^3
+    assert np.all(np.abs(d.cpu().numpy() - rd) <= TOL * np.maximum(1.0, np.abs(rd)) + 2.0 * t_far * band)
+    print(f"c1 f4: max |d alpha| {np.abs(a.cpu().numpy() - ra).max():.2e}, band p50 {np.median(band):.1e} "
+          f"max {band.max():.1e}")
     got = po.po_leaf_max_alpha(tree, r, gamma=0.01).cpu().numpy()
-    want = om.leaf_max_alpha(ot, rays.astype(np.float64), gamma=0.01)
-    assert np.abs(got - want).max() <= 2e-3
+    want = om.leaf_max_alpha(ot, rays, gamma=0.01)
+    assert np.abs(got - want).max() <= TOL + band.max()
     assert ((got > 0) == (want > 0)).mean() > 0.999
 
 

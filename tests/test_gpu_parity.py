@@ -37,6 +37,19 @@ def _tie_free(om, ot, rays, gamma):
     return om.tie_flags(ot, rays, gamma=gamma if gamma > 0 else 1e-30) == 0
 
 
+def _check_rgb(om, ot, rays, gamma, got, ref, min_tie_free):
+    """RGB parity of one ray set: tie-free rays (reading Q27) within RGB_TOL, every excluded ray
+    within the oracle's error-propagation bound for it (+ RGB_TOL).  Returns the tie-free mask."""
+    f, bound = om.tie_flags(ot, rays, gamma=gamma if gamma > 0 else 1e-30, with_bound=True)
+    ok = f == 0
+    assert ok.mean() >= min_tie_free, f"only {ok.sum()} of {ok.size} rays tie-free"
+    err = np.abs(np.asarray(got, np.float64) - ref).max(axis=1)
+    assert err[ok].max(initial=0.0) <= RGB_TOL, err[ok].max()
+    bad = np.flatnonzero(err > bound + RGB_TOL)
+    assert bad.size == 0, [(int(i), float(err[i]), float(bound[i]), int(f[i])) for i in bad[:5]]
+    return ok
+
+
 def _grad_ok(a, b, tag):
     a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
     rel = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
@@ -58,12 +71,7 @@ def test_c0_render_camera(env, c0_tree, gamma):
     ot = om.OracleTree(c0_tree)
     rays = om.camera_rays(cam, W, H)
     ref = om.render(ot, rays, gamma=gamma)
-    ok = _tie_free(om, ot, rays, gamma)
-    assert ok.sum() > 4000
-    err = np.abs(img[ok] - ref["rgb"][ok]).max()
-    assert err <= RGB_TOL, err
-    # rays excluded as ties still render sanely
-    assert np.abs(img - ref["rgb"]).max() <= 0.02
+    _check_rgb(om, ot, rays, gamma, img, ref["rgb"], 0.99)
 
 
 @pytest.mark.parametrize("gamma", [0.01, 0.0])
@@ -208,7 +216,8 @@ def test_fp16_payload(env, deg):
 
 
 def test_c1_sampled_pixels_full_launch(env, c1_tree):
-    """c1 at full size in the bench's launch configuration; oracle on 4096 sampled pixels."""
+    """c1 at full size in the bench's launch configuration; oracle on 4096 sampled pixels: >= 95 %
+    of them tie-free and within 1e-4, every excluded one within its tie bound (reading Q27)."""
     po, om, torch = env
     tree = po.tree_from_gen(c1_tree)
     cam, W, H = gen.config_camera("c1")
@@ -217,16 +226,64 @@ def test_c1_sampled_pixels_full_launch(env, c1_tree):
     pick = rng(17).choice(W * H, 4096, replace=False)
     ot = om.OracleTree(c1_tree)
     ref = om.render(ot, rays[pick], gamma=0.01)
-    ok = _tie_free(om, ot, rays[pick], 0.01)
-    # at depth 9 ~27% of rays have two plane crossings within 1e-6*edge (reading Q27 (i))
-    assert ok.sum() > 2500
-    assert np.abs(img[pick][ok] - ref["rgb"][ok]).max() <= RGB_TOL
+    ok = _check_rgb(om, ot, rays[pick], 0.01, img[pick], ref["rgb"], 0.95)
     print(f"c1 sample: {ok.sum()} tie-free of 4096, all-ray max err {np.abs(img[pick] - ref['rgb']).max():.3e}")
     # whole-frame property: every pixel is a convex combination of colours in (0,1) and white
     assert np.all(img >= 0) and np.all(img <= 1.0 + 1e-6)
     # counters of the same traversal match the oracle's per-ray counts on the sample
     st = po.po_render_stats(tree, po.cams_tensor(cam), W, H)
     assert st["hit_rays"] > 0.3 * W * H
+
+
+def test_c1_trace_bit_exact_production_traversal(env, c1_tree):
+    """The leaf sequence the product kernels walk (the level-(D-1) cell index) on 8192 rays of the
+    c1 bench view, bit-exact against the oracle on tie-free rays (>= 95 % of them); the same rays
+    fed to both sides (the GPU's fp32 camera rays)."""
+    po, om, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    assert tree.index_bytes() == 4 * 256 ** 3
+    cam, W, H = gen.config_camera("c1")
+    rays = po.po_camera_rays(po.cams_tensor(cam), W, H).reshape(-1, 6)
+    pick = torch.from_numpy(rng(18).choice(W * H, 8192, replace=False)).cuda()
+    r = rays[pick].contiguous()
+    ids, counts, _ = po.po_trace(tree, r, max_leaves=64, gamma=0.01, with_nodes=False)
+    r64 = r.cpu().numpy().astype(np.float64)
+    ot = om.OracleTree(c1_tree)
+    ref = om.render(ot, r64, gamma=0.01, max_leaves=64)
+    ok = _tie_free(om, ot, r64, 0.01)
+    assert ok.mean() >= 0.95, ok.sum()
+    assert (ref["n_proc"][ok] > 0).sum() > 2000   # the sample hits the object
+    np.testing.assert_array_equal(counts.cpu().numpy()[ok], ref["n_proc"][ok])
+    np.testing.assert_array_equal(ids.cpu().numpy()[ok], ref["leaf_ids"][ok])
+
+
+@pytest.mark.parametrize("case", ["random4", "random7", "coarse", "c1"])
+def test_production_traversal_equals_classic(env, c1_tree, case):
+    """The cell-index traversal (every product kernel) and the classic descent from the deepest
+    common ancestor (trees without an index) walk the same boxes with the same fp32 t values:
+    identical leaf sequences on EVERY ray, ties included, and bit-identical po_render_rays
+    colours between a tree with the index and the same tree built with PO_TREE_NO_INDEX.  The random
+    trees are mixed-depth; 'coarse' has mostly data leaves above depth D - 1, which the index
+    hands to the classic path."""
+    po, om, torch = env
+    if case == "c1":
+        t = c1_tree
+        cam, W, H = gen.config_camera("c1", 3)
+        rays = po.po_camera_rays(po.cams_tensor(cam), W, H).reshape(-1, 6)[::7].contiguous()
+    else:
+        depth, p_split = {"random4": (4, 0.55), "random7": (7, 0.55), "coarse": (6, 0.3)}[case]
+        t = gen.scene_random(100 + depth, depth=depth, sh_degree=1, sigma_scale=3.0, p_split=p_split)
+        rays = _dev(torch, gen.random_rays(101, 20000, inside_frac=0.15))
+    tree = po.tree_from_gen(t)
+    plain = po.tree_from_gen(t, index=False)
+    assert plain.index_bytes() == 0 and tree.index_bytes() > 0
+    for gamma in (0.01, 0.0):
+        a = po.po_trace(tree, rays, max_leaves=48, gamma=gamma, with_nodes=False)
+        b = po.po_trace(tree, rays, max_leaves=48, gamma=gamma, with_nodes=False, classic=True)
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        ca = po.po_render_rays(tree, rays, gamma=gamma)
+        cb = po.po_render_rays(plain, rays, gamma=gamma)
+        assert torch.equal(ca, cb)
 
 
 def test_stats_match_oracle_c0(env, c0_tree):

@@ -155,11 +155,86 @@ def test_full_tree_deltas_sum_to_chord(oracle_mod, depth):
             assert abs((b - a).sum() - (ch[1] - ch[0])) < 1e-12
 
 
-def test_tie_flags_detect_constructed_ties(oracle_mod):
-    t = gen.scene_random(3, depth=4, sh_degree=0)
-    ot = oracle_mod.OracleTree(t)
+def _octant0_tree():
+    """Depth 2 in [-1,1]^3: root octant 0 ([-1,0)^3) holds 8 leaves (sigma~ 2), the other 7
+    octants are empty boxes."""
+    from conftest import make_tree
+    L, I = 2 << 30, 1 << 30
+    child = [[I | 1] + [0] * 7, [L | k for k in range(8)]]
+    return make_tree(child, np.full(8, 2.0), np.zeros((8, 1, 3)), 2, 0)
+
+
+def test_tie_bit0_only_where_a_leaf_touches_the_crossing(oracle_mod):
+    """Reading Q27 (i): a ray along the x = y diagonal crosses an x plane and a y plane at the same
+    t at every plane.  At z = 0.3 every cell around those crossings is empty (no leaf can be
+    entered or skipped: not a tie); at z = -0.3 the crossings at (-0.5, -0.5) and (0, 0) touch
+    the leaves of octant 0 (a tie)."""
+    ot = oracle_mod.OracleTree(_octant0_tree())
     d = np.array([1.0, 1.0, 0.0]) / np.sqrt(2)
-    edge_ray = np.concatenate([[-3.0, -3.0, 0.3], d])            # crosses x and y planes together
-    clean = np.array([-3.0, 0.1037, 0.2113, 1.0, 0.0123, 0.0371])
-    f = oracle_mod.tie_flags(ot, np.stack([edge_ray, clean]))
-    assert f[0] & 1 and f[1] == 0
+    empty = np.concatenate([[-3.0, -3.0, 0.3], d])
+    leafy = np.concatenate([[-3.0, -3.0, -0.3], d])
+    clean = np.array([-3.0, -0.6037, -0.2113, 1.0, 0.0123, 0.0371])
+    f = oracle_mod.tie_flags(ot, np.stack([empty, leafy, clean]), gamma=0.0)
+    assert f[0] == 0 and f[1] & 1 and f[2] == 0
+
+
+def test_tie_bit1_sliver_segment(oracle_mod):
+    """A ray 1e-9 off the edge x = y = -0.5 (inside octant 0's leaves) cuts a sliver of length
+    ~3e-9 out of one leaf: shorter than the fp32 error of its two ends."""
+    ot = oracle_mod.OracleTree(_octant0_tree())
+    d = np.array([1.0, 1.0, 0.0]) / np.sqrt(2)
+    r = np.concatenate([[-3.0, -3.0 + 2e-9, -0.3], d])
+    leaves, a, b, _ = oracle_mod.trace_ray(ot, r)
+    assert (b - a).min() < 1e-8      # the sliver is really there
+    f = oracle_mod.tie_flags(ot, r[None], gamma=0.0)
+    assert f[0] & 2
+
+
+def test_tie_bit2_transmittance_at_gamma_and_bound(oracle_mod):
+    """Full depth-1 tree, a ray along +x at y = -0.37, z = 0.21 crosses two unit-length leaves:
+    T_1 = exp(-sigma).  sigma = ln(1/gamma) puts T_1 on gamma (a tie; the bound then allows a
+    termination flip: >= gamma); sigma = 1 keeps T far from gamma (no tie, bound = the optical
+    depth error only)."""
+    from conftest import full_depth1
+    gamma = 0.01
+    r = np.array([[-3.0, -0.37, 0.21, 1.0, 0.0, 0.0]])
+    t_tie = oracle_mod.OracleTree(full_depth1(np.log(1.0 / gamma)))
+    f, b = oracle_mod.tie_flags(t_tie, r, gamma=gamma, with_bound=True)
+    assert f[0] == 4 and b[0] >= gamma
+    t_ok = oracle_mod.OracleTree(full_depth1(1.0))
+    f, b = oracle_mod.tie_flags(t_ok, r, gamma=gamma, with_bound=True)
+    assert f[0] == 0 and 0 < b[0] < 3e-5
+
+
+def test_tie_bit3_origin_on_a_plane(oracle_mod):
+    from conftest import full_depth1
+    ot = oracle_mod.OracleTree(full_depth1(1.0))
+    on = np.array([0.0, 0.13, 0.21, 0.3, 0.5, 0.7])
+    off = np.array([0.013, 0.13, 0.21, 0.3, 0.5, 0.7])
+    f = oracle_mod.tie_flags(ot, np.stack([on, off]), gamma=0.0)
+    assert f[0] & 8 and not (f[1] & 8)
+
+
+@pytest.mark.parametrize("which", ["random", "c0"])
+def test_tie_bound_covers_rounding_of_the_ray(oracle_mod, c0_tree, which):
+    """The per-ray bound of reading Q27 holds for the oracle itself: rendering each ray rounded
+    to fp32 (a perturbation of the size any fp32 implementation sees) instead of the double ray
+    changes C by at most the bound of the tie rays (+ 1e-5 for the smooth change of tie-free
+    rays), and tie-free rays keep their leaf sequence."""
+    if which == "c0":
+        t = c0_tree
+        cam, W, H = gen.config_camera("c0")
+        rays = oracle_mod.camera_rays(cam, W, H)
+    else:
+        t = gen.scene_random(77, depth=5, sh_degree=1, sigma_scale=20.0)
+        rays = _rays(78, 3000)
+    ot = oracle_mod.OracleTree(t)
+    r32 = rays.astype(np.float32).astype(np.float64)
+    for gamma in (0.01, 0.0):
+        f, b = oracle_mod.tie_flags(ot, rays, gamma=max(gamma, 1e-30), with_bound=True)
+        a = oracle_mod.render(ot, rays, gamma=gamma, max_leaves=128)
+        c = oracle_mod.render(ot, r32, gamma=gamma, max_leaves=128)
+        diff = np.abs(a["rgb"] - c["rgb"]).max(axis=1)
+        assert np.all(diff <= b + 1e-5)
+        ok = f == 0
+        assert np.array_equal(a["leaf_ids"][ok], c["leaf_ids"][ok])
