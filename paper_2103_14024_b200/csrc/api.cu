@@ -59,13 +59,17 @@ struct po_tree {
     unsigned* d_work = nullptr;
     std::mutex work_mu;
     std::vector<cudaStream_t> work_streams;
+    int slot_of(cudaStream_t s) {   // caller holds work_mu
+        for (size_t i = 0; i < work_streams.size(); ++i)
+            if (work_streams[i] == s) return (int)i;
+        if ((int)work_streams.size() >= kWorkSlots) return -1;
+        work_streams.push_back(s);
+        return (int)work_streams.size() - 1;
+    }
     unsigned* work_for(cudaStream_t s) {
         std::lock_guard<std::mutex> lk(work_mu);
-        for (size_t i = 0; i < work_streams.size(); ++i)
-            if (work_streams[i] == s) return d_work + kWorkStride * i;
-        if ((int)work_streams.size() >= kWorkSlots) return nullptr;
-        work_streams.push_back(s);
-        return d_work + kWorkStride * (work_streams.size() - 1);
+        const int i = slot_of(s);
+        return i < 0 ? nullptr : d_work + kWorkStride * i;
     }
     int* sgd_flag() { return reinterpret_cast<int*>(d_work + kWorkStride * kWorkSlots); }
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)

@@ -742,26 +742,87 @@ __global__ void __launch_bounds__(256, 2) k_backward(DevTree tr, const float* __
 // then every lane applies GradVisitor::seg's formula to its own segment.  Rays whose segments
 // overflowed (count > max_seg) are left to k_backward<..., true>.
 // Where the replay puts each segment's gradient: atomically into the leaf rows (default), or as
-// a record for the deterministic segmented reduction (po_render_backward_deterministic).
+// a record for the deterministic segmented reduction (po_render_backward_deterministic).  Sinks
+// are called by the whole warp once per round of up to 32 segments (lane l holds segment
+// base + l when `act`); the active lanes are 0..n-1.
+//
+// Row reductions, lane-cooperative (SH-1 / SH-3: rows of 3B = 12 / 48 floats, whole float4
+// quads).  A lane-per-segment red.v4 loop sends every lane to a different 192-B row, so each of
+// the 12 red instructions of a round is 32 scattered L1 wavefronts (the replay's bound, r01:
+// issue-active 17 %).  Instead the round's n segments x QPR quads are flattened and dealt to the
+// 32 lanes in order: quad q = 32 it + lane belongs to segment q / QPR and row quad q % QPR, so one
+// red.v4 instruction covers 512 contiguous bytes of ~3 consecutive-segment rows.  A lane's quad
+// index cycles through 3 values (32 it mod QPR), so its basis values and channel selectors are
+// three precomputed sets; the segment's gz comes by shuffle.  Same per-element products
+// gz[ch] * Y[b] (scaled by `scale`), only the order of the atomic adds changes.
+template <int DEG>
+struct CoopRows {
+    static constexpr int NE = 3 * ShDim<DEG>::B;
+    static constexpr int QPR = NE / 4;   // quads per row
+    static constexpr bool kCoop = (NE % 4) == 0;
+    float yv[3][4];   // [phase][k]: Y of element 4 qq + k
+    int ch[3][4];     // its channel
+    int qq[3];
+    __device__ __forceinline__ CoopRows(const float* Y, float scale) {
+        if constexpr (kCoop) {
+            const int lane = threadIdx.x & 31;
+            // lane b holds Y[b] (a sum of 0/1-masked terms: no register array is indexed by the
+            // lane, which would put Y in local memory); lanes then fetch Y[el / 3] by shuffle
+            float ydist = 0.f;
+#pragma unroll
+            for (int b = 0; b < ShDim<DEG>::B; ++b) ydist = fmaf(Y[b], (float)(lane == b), ydist);
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+                qq[p] = (lane + 32 * p) % QPR;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int el = 4 * qq[p] + k;
+                    yv[p][k] = scale * __shfl_sync(0xffffffffu, ydist, el / 3);
+                    ch[p][k] = el % 3;
+                }
+            }
+        }
+    }
+    // rows of `stride` floats at base; active lanes 0..n-1 hold (idx, gz)
+    __device__ __forceinline__ void add(float* __restrict__ base, int64_t stride, int n, uint32_t idx,
+                                        const float gz[3]) const {
+        const int lane = threadIdx.x & 31;
+        const int total = n * QPR;
+        for (int it0 = 0; it0 * 32 < total; it0 += 3) {
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+                const int q = (it0 + p) * 32 + lane;
+                const int sgi = min(q / QPR, 31);
+                const uint32_t id = __shfl_sync(0xffffffffu, idx, sgi);
+                const float g0 = __shfl_sync(0xffffffffu, gz[0], sgi);
+                const float g1 = __shfl_sync(0xffffffffu, gz[1], sgi);
+                const float g2 = __shfl_sync(0xffffffffu, gz[2], sgi);
+                if (q < total) {
+                    float v[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v[k] = (ch[p][k] == 0 ? g0 : (ch[p][k] == 1 ? g1 : g2)) * yv[p][k];
+                    float* a = base + (size_t)id * stride + 4 * qq[p];
+                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v[0]), "f"(v[1]),
+                                 "f"(v[2]), "f"(v[3])
+                                 : "memory");
+                }
+            }
+        }
+    }
+};
+
 template <int DEG>
 struct AtomicSink {
     float* __restrict__ grad_sigma;
     float* __restrict__ grad_sh;
-    __device__ __forceinline__ void operator()(int32_t, uint32_t idx, float gsig, const float gz[3], const float* Y) {
+    __device__ __forceinline__ void round(const CoopRows<DEG>& rows, int32_t, bool act, int n, uint32_t idx, float gsig,
+                                          const float gz[3], const float* Y) {
         constexpr int NE = 3 * ShDim<DEG>::B;
-        atomicAdd(grad_sigma + idx, gsig);
-        float* row = grad_sh + (size_t)idx * NE;
-        if constexpr (NE % 4 == 0) {
-#pragma unroll
-            for (int j = 0; j < NE / 4; ++j) {
-                float v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3];
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * j), "f"(v[0]),
-                             "f"(v[1]), "f"(v[2]), "f"(v[3])
-                             : "memory");
-            }
-        } else {
+        if (act) atomicAdd(grad_sigma + idx, gsig);
+        if constexpr (CoopRows<DEG>::kCoop) {
+            rows.add(grad_sh, NE, n, idx, gz);
+        } else if (act) {
+            float* row = grad_sh + (size_t)idx * NE;
 #pragma unroll
             for (int el = 0; el < NE; ++el) atomicAdd(row + el, gz[el % 3] * Y[el / 3]);
         }
@@ -775,7 +836,10 @@ struct EmitSink {   // segment k of ray `ray` -> flat slot f0 + k
     int32_t* __restrict__ ray_of;
     int64_t f0;
     int32_t ray;
-    __device__ __forceinline__ void operator()(int32_t k, uint32_t idx, float gsig, const float gz[3], const float*) {
+    template <class R>
+    __device__ __forceinline__ void round(const R&, int32_t k, bool act, int, uint32_t idx, float gsig,
+                                          const float gz[3], const float*) {
+        if (!act) return;
         const int64_t f = f0 + k;
         key[f] = idx;
         val[f] = (uint32_t)f;
@@ -787,7 +851,7 @@ struct EmitSink {   // segment k of ray `ray` -> flat slot f0 + k
 template <int DEG, class Sink>
 __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __restrict__ rays, int64_t i,
                                            const float* __restrict__ dL_dC, const double* __restrict__ aux,
-                                           const SegIn& si, Sink& sink) {
+                                           const SegIn& si, Sink& sink, float row_scale) {
     constexpr int B = ShDim<DEG>::B;
     const int lane = threadIdx.x & 31;
     const int32_t ns = __ldg(si.count + i);
@@ -801,6 +865,7 @@ __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __res
     if (!unit_direction(dir, d)) return;
     float Y[B];
     ray_basis<DEG>(tr, d, Y);
+    const CoopRows<DEG> rows(Y, row_scale);
     double Ctot[3], carry[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) Ctot[ch] = aux[i * 4 + ch];
@@ -826,7 +891,6 @@ __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __res
             P[ch] = carry[ch] + v;
             carry[ch] = __shfl_sync(0xFFFFFFFFu, P[ch], 31);
         }
-        if (!act) continue;
         const uint32_t idx = __float_as_uint(a.x);
         const float delta = a.y, w = a.z, Tn = a.w;
         double acc = 0.0;
@@ -834,8 +898,8 @@ __device__ __forceinline__ void replay_ray(const DevTree& tr, const float* __res
         for (int ch = 0; ch < 3; ++ch) acc += (double)g[ch] * ((double)c[ch] * (double)Tn - (Ctot[ch] - P[ch]));
         float gz[3];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) gz[ch] = g[ch] * w * c[ch] * (1.f - c[ch]);
-        sink(k, idx, (float)((double)delta * acc), gz, Y);
+        for (int ch = 0; ch < 3; ++ch) gz[ch] = act ? g[ch] * w * c[ch] * (1.f - c[ch]) : 0.f;
+        sink.round(rows, k, act, min(ns - base, 32), idx, (float)((double)delta * acc), gz, Y);
     }
 }
 
@@ -848,7 +912,7 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay(DevTree tr, const fl
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= n) return;
     AtomicSink<DEG> sink{grad_sigma, grad_sh};
-    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink, 1.f);
 }
 
 // a8 + a9 fused (po_render_backward_sgd, one replica): each segment's contribution scaled by
@@ -861,21 +925,14 @@ struct SgdSink {
     float* __restrict__ sh;
     int32_t sh_row;
     float neg_lr;
-    __device__ __forceinline__ void operator()(int32_t, uint32_t idx, float gsig, const float gz[3], const float* Y) {
+    __device__ __forceinline__ void round(const CoopRows<DEG>& rows, int32_t, bool act, int n, uint32_t idx, float gsig,
+                                          const float gz[3], const float* Y) {
         constexpr int NE = 3 * ShDim<DEG>::B;
-        atomicAdd(sigma + idx, neg_lr * gsig);
-        float* row = sh + (size_t)idx * sh_row;
-        if constexpr (NE % 4 == 0) {
-#pragma unroll
-            for (int j = 0; j < NE / 4; ++j) {
-                float v[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = neg_lr * (gz[(4 * j + q) % 3] * Y[(4 * j + q) / 3]);
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + 4 * j), "f"(v[0]),
-                             "f"(v[1]), "f"(v[2]), "f"(v[3])
-                             : "memory");
-            }
-        } else {
+        if (act) atomicAdd(sigma + idx, neg_lr * gsig);
+        if constexpr (CoopRows<DEG>::kCoop) {
+            rows.add(sh, sh_row, n, idx, gz);   // rows were built with scale = -lr
+        } else if (act) {
+            float* row = sh + (size_t)idx * sh_row;
 #pragma unroll
             for (int el = 0; el < NE; ++el) atomicAdd(row + el, neg_lr * (gz[el % 3] * Y[el / 3]));
         }
@@ -891,7 +948,7 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay_sgd(DevTree tr, cons
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= n) return;
     SgdSink<DEG> sink{sigma, sh, sh_row, neg_lr};
-    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink, neg_lr);
 }
 
 // the same over one chunk of a po_backward_plan (bounds on the device): a persistent grid
@@ -909,7 +966,8 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay_chunk(DevTree tr, co
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     AtomicSink<DEG> sink{grad_sigma, grad_sh};
-    for (int64_t j = b + w0; j < e; j += nw) replay_ray<DEG>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, sink);
+    for (int64_t j = b + w0; j < e; j += nw)
+        replay_ray<DEG>(tr, rays, (int64_t)__ldg(perm + j), dL_dC, aux, si, sink, 1.f);
 }
 
 // ---- deterministic pass 2: segmented reduction into leaves (NEXT f2 "deterministic-reduction
@@ -951,7 +1009,7 @@ __global__ void __launch_bounds__(256, 3) k_det_emit(DevTree tr, const float* __
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= n) return;
     EmitSink sink{key, val, contrib, ray_of, (int64_t)__ldg(offs + i), (int32_t)i};
-    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink);
+    replay_ray<DEG>(tr, rays, i, dL_dC, aux, si, sink, 1.f);
 }
 
 template <int DEG>

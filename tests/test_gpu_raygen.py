@@ -42,14 +42,28 @@ def test_camera_rays_bit_exact(env):
 
 
 def test_render_equals_render_rays_of_camera_rays(env, c1_tree):
+    """po_render (persistent k_render with tail balancing: paused rays handed to other warps and
+    resumed from their pixel, cell and (T, C)) equals po_render_rays of the same camera rays bit
+    for bit: one 3-view launch, then single-view launches back to back on one stream (the queue
+    and its ready flags are reused across launches) and on a second stream."""
     po, torch = env
     tree = po.tree_from_gen(c1_tree)
-    cams = np.concatenate([gen.config_camera("c1", v)[0] for v in range(3)])
+    cams = np.concatenate([gen.config_camera("c1", v)[0] for v in range(8)])
     ct = po.cams_tensor(cams)
-    img = po.po_render(tree, ct, 800, 800)
     rays = po.po_camera_rays(ct, 800, 800).reshape(-1, 6)
-    img2 = po.po_render_rays(tree, rays).reshape(img.shape)
-    assert torch.equal(img, img2)
+    ref = po.po_render_rays(tree, rays).reshape(8, 800, 800, 3)
+    img = po.po_render(tree, ct[:3], 800, 800)
+    assert torch.equal(img, ref[:3])
+    side = torch.cuda.Stream()
+    for rep in range(2):
+        for v in range(8):
+            if rep == 1 and v % 2:
+                with torch.cuda.stream(side):
+                    one = po.po_render(tree, ct[v:v + 1], 800, 800, stream=side)
+                side.synchronize()
+            else:
+                one = po.po_render(tree, ct[v:v + 1], 800, 800)
+            assert torch.equal(one[0], ref[v]), (rep, v)
 
 
 def test_tile_shards_assemble_the_frame():

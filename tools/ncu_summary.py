@@ -23,7 +23,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__cycles_active.avg", "gpc__cycles_elapsed.max", "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
         "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct", "smsp__warp_issue_stalled_no_instruction_per_warp_active.pct",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "local_load_bytes", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum"]
+        "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "local_load_bytes", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum",
+        "lts__t_sectors.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum",
+        "smsp__warp_issue_stalled_mio_throttle_per_warp_active.pct", "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
+        "smsp__warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_active",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
 
 
 def launches(path):
@@ -100,10 +104,11 @@ def main():
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             by = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
+            lts = mb("lts__t_bytes.sum") if "lts__t_bytes.sum" in d else None
             wl = os.environ.get("NCU_WORKLOAD", "c1")   # which bench workload the capture is of
             what = {"c1": "one c1 frame", "c2": "one c2 launch (200 views)", "c3": "one c3 frame"}.get(wl, wl)
             name = "ncu_render_summary.json" if wl == "c1" else f"ncu_render_summary_{wl}.json"
-            json.dump({"dram_bytes_per_launch": by, "source": f"profiles/{tag}_{kern}_ncu.md (ncu --set full, {what}, cold L2)",
+            json.dump({"dram_bytes_per_launch": by, "lts_bytes_per_launch": lts, "source": f"profiles/{tag}_{kern}_ncu.md (ncu --set full, {what}, cold L2)",
                        "duration": d["gpu__time_duration.sum"]},
                       open(os.path.join(ROOT, "profiles", name), "w"), indent=1)
 

@@ -1,4 +1,5 @@
-"""Scheduling analysis of one c1 frame: per-tile start/end times from po_render_timeline."""
+"""Scheduling analysis of one c1 frame: per-tile start/end times from po_render_timeline.
+Needs a diagnostics build: PO_NVCC_EXTRA=-DPO_DIAG (po_render_timeline is refused otherwise)."""
 import os
 import sys
 
@@ -21,6 +22,8 @@ torch.cuda.synchronize()
 img, tl = po.po_render_timeline(tree, cams[6 * V:7 * V], 800, 800)
 torch.cuda.synchronize()
 tl = tl.cpu().numpy().astype(np.int64)
+handed = (tl[:, 3] >> 32)
+print(f"rays handed to helper warps: {int(handed.sum())} from {int((handed > 0).sum())} tiles")
 t0, t1 = tl[:, 0], tl[:, 1]
 sm = tl[:, 2] >> 32
 ok = t0 > 0
