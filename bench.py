@@ -143,14 +143,16 @@ def _workload_desc(tree_gen, wl="c1", ws=1):
                          f"i = r (mod {ws}) in ONE launch",
                 "l2": "flushed (256 MiB write) before every timed step; only the render is inside the CUDA events",
                 "global_batch": "200 views per step (all ranks)"}
-    if wl == "c3":
-        return {"workload": "c3: Tanks&Temples-shaped bounded scene, depth-10 sparse octree (1024^3), "
-                            f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp16 payload (sigma fp32), "
+    if wl in ("c3", "c3sh25"):
+        deg = "SH-25 (l = 4, P:587-588)" if wl == "c3sh25" else "SH-3"
+        return {"workload": f"{wl}: Tanks&Temples-shaped bounded scene, depth-10 sparse octree (1024^3), "
+                            f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, {deg} fp16 payload (sigma fp32), "
                             "1920x1080, gamma 0.01",
                 "views": "orbit r 2.6, el 15 deg, az = 20 + 1.8*i deg, f 1400 px; rank r renders views r, r+N, ...",
                 "l2": "flushed (256 MiB write) before every timed step; only the render is inside the CUDA events",
                 "global_batch": "1 frame per rank per step"}
-    return {"workload": "c1: NeRF-synthetic-shaped SDF object, depth-9 sparse octree (512^3), "
+    thick = " thick shell sdf/h in (-8, +1) (SURVEY 8(d) paper-scale variant, P:669 mean 1.93 GB)," if wl == "c1thick" else ""
+    return {"workload": f"{wl}: NeRF-synthetic-shaped SDF object, depth-9 sparse octree (512^3),{thick} "
                         f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp32 payload, 800x800, gamma 0.01",
             "views": "c1 orbit, az = 37 + 1.8*i deg, el 30 deg, r 3.4, f 1111.1 px; rank r renders views r, r+N, ...",
             "l2": "flushed (256 MiB write) before every timed step; only the render is inside the CUDA events",
@@ -164,9 +166,12 @@ def run_ours(args):
     import paper_2103_14024_b200 as po
 
     wl = args.workload
-    W, H = (1920, 1080) if wl == "c3" else (800, 800)
-    payload = po.PO_F16 if wl == "c3" else po.PO_F32
+    c3like = wl.startswith("c3")
+    W, H = (1920, 1080) if c3like else (800, 800)
+    payload = po.PO_F16 if c3like else po.PO_F32
     metric = {"c3": "1920x1080 FPS, SH-3 depth-10 fp16 PlenOctree (c3)",
+              "c3sh25": "1920x1080 FPS, SH-25 depth-10 fp16 PlenOctree (c3 scene at the paper's T&T basis)",
+              "c1thick": "800x800 FPS, SH-3 512^3 PlenOctree, thick shell (paper-scale tree)",
               "c2": "views/s, 200-view 800x800 orbit, SH-3 512^3 PlenOctree (c2)"}.get(wl, METRIC)
     unit = "views/s" if wl == "c2" else UNIT
     ws, rank, local = _dist()
@@ -175,7 +180,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     po.lib()
-    t_gen = gen.scene_c3() if wl == "c3" else gen.scene_c1()
+    t_gen = {"c3": lambda: gen.scene_c3(), "c3sh25": lambda: gen.scene_c3(sh_degree=4),
+             "c1thick": lambda: gen.scene_c1(thick=True)}.get(wl, lambda: gen.scene_c1())()
     tree = po.tree_from_gen(t_gen, payload=payload, device=local)
     if wl == "c2":
         # every step renders the whole 200-view orbit: rank r takes views r, r+N, ... in one launch
@@ -186,13 +192,14 @@ def run_ours(args):
     else:
         V = max(1, args.views_per_launch)
         n_views = max(args.steps + args.warmup, 1) * ws * V
-        cam_recs = np.concatenate([gen.config_camera(wl, v)[0] for v in range(n_views)])
+        cam_cfg = "c3" if c3like else ("c1" if wl == "c1thick" else wl)
+        cam_recs = np.concatenate([gen.config_camera(cam_cfg, v)[0] for v in range(n_views)])
     cams = po.cams_tensor(cam_recs, dev)
     out = torch.empty((V, H, W, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    tile_shard = args.shard == "tile" and wl in ("c1", "c3")
+    tile_shard = args.shard == "tile" and wl in ("c1", "c3", "c1thick", "c3sh25")
 
     def view_of(step):   # first of the V consecutive views rank `rank` renders at `step`
         if wl == "c2":
@@ -229,7 +236,7 @@ def run_ours(args):
             stats[k] += st[k] * (args.steps if wl == "c2" else 1)   # c2: every step renders the same orbit
     K = max(args.steps, 1)
     alg_bytes = (stats["leaf_visits"] * rec_bytes + stats["nodes"] * 32) / K + W * H * 12 * V
-    if args.shard == "tile" and wl in ("c1", "c3"):
+    if tile_shard:
         alg_bytes /= ws   # each rank renders 1/N of the blocks (interleaved: an even share)
 
     for s in range(args.warmup):
@@ -343,7 +350,7 @@ def run_ours(args):
                                                                   4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": f"po::k_render<3,{int(payload == po.PO_F16)}>", "peak_source": peak_src,
+                         "kernel": f"po::k_render<{t_gen.sh_degree},{int(payload == po.PO_F16)}>", "peak_source": peak_src,
                          "alg_bytes_per_launch": round(alg_bytes),
                          "alg_bytes_def": f"SURVEY 8(d) ALG_RAY: leaf visits*{rec_bytes} B record + internal nodes "
                                           "met (classic descent)*32 B + 12 B/pixel out",
@@ -601,7 +608,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4"], default="c1")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c1thick", "c3sh25"], default="c1")
     ap.add_argument("--shard", choices=["view", "tile"], default="view",
                     help="c1/c3 at N>1: views per rank (weak) or the blocks of one view per rank (strong)")
     ap.add_argument("--views-per-launch", type=int, default=1,

@@ -230,20 +230,22 @@ def _scene_c1(seed: int, thick: bool) -> Tree:
                 np.full(cells.shape[0], depth, np.int32), cells)
 
 
-def scene_c3(seed: int = 0) -> Tree:
-    """c3: Tanks&Temples-shaped bounded scene, depth-10 sparse octree, SH-3 (fp16 payload at upload)."""
-    return _cached(f"c3_s{seed}", lambda: _scene_c3(seed))
+def scene_c3(seed: int = 0, sh_degree: int = 3) -> Tree:
+    """c3: Tanks&Temples-shaped bounded scene, depth-10 sparse octree, SH-3 (fp16 payload at upload);
+    sh_degree=4 is the paper's own T&T setting, SH-25 (NEXT f3)."""
+    key = f"c3_s{seed}" if sh_degree == 3 else f"c3_s{seed}_l{sh_degree}"
+    return _cached(key, lambda: _scene_c3(seed, sh_degree))
 
 
-def _scene_c3(seed: int) -> Tree:
+def _scene_c3(seed: int, sh_degree: int = 3) -> Tree:
     depth = 10
     cells = shell_cells(sdf_c3, depth, -3.0, 1.0)
     child, order = build_from_leaf_cells(cells, depth)
     cells = cells[order]
     size = EDGE / (1 << depth)
     vals = sdf_c3(BBOX_MIN.astype(np.float64) + (cells + 0.5) * size)
-    sigma, sh = _payload_c1(_rng(seed), cells, depth, vals, 3, sigma_peak=1536.0)
-    return Tree(depth, BBOX_MIN.copy(), EDGE, 3, child, sigma, sh,
+    sigma, sh = _payload_c1(_rng(seed), cells, depth, vals, sh_degree, sigma_peak=1536.0)
+    return Tree(depth, BBOX_MIN.copy(), EDGE, sh_degree, child, sigma, sh,
                 np.full(cells.shape[0], depth, np.int32), cells)
 
 

@@ -58,10 +58,11 @@ typedef struct {
 } po_tree_desc;
 
 /* po_tree_desc.flags.  By default po_tree_create also builds the tree's dense level-(D-1) cell
- * index (D in 2..10): one uint32 per cell of the 2^(D-1)-per-axis grid, 4 * 8^(D-1) bytes
- * (67 MB at D = 9, 537 MB at D = 10; po_tree_index_bytes), through which every traversal
- * kernel finds the box that contains a cell with one or two loads instead of a re-descent
- * (same boxes and t values, bit-identical results).  PO_TREE_NO_INDEX skips it (every kernel
+ * index (D in 2..10): 8 bytes per cell of the 2^(D-1)-per-axis grid, 8 * 8^(D-1) bytes
+ * (134 MB at D = 9, 1.07 GB at D = 10; po_tree_index_bytes), through which every traversal
+ * kernel finds the box that contains a cell with one load (two for a depth-(D-1) node whose
+ * leaves are not numbered consecutively in octant order) instead of a re-descent (same boxes
+ * and t values, bit-identical results).  PO_TREE_NO_INDEX skips it (every kernel
  * then descends from the deepest common ancestor).  Nothing is built later: renders and
  * backward calls never allocate or synchronise for it. */
 enum { PO_TREE_NO_INDEX = 1 };

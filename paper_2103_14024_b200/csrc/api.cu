@@ -73,7 +73,7 @@ struct po_tree {
     }
     int* sgd_flag() { return reinterpret_cast<int*>(d_work + kWorkStride * kWorkSlots); }
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
-    uint32_t* d_grid = nullptr;      // dense level-(D-1) cell index (build_grid, at po_tree_create)
+    uint2* d_grid = nullptr;         // dense level-(D-1) cell index (build_grid, at po_tree_create)
     size_t grid_bytes = 0;
     // po_render_host holds this for its whole body (camera / image / pipeline scratch)
     std::mutex host_mu;
@@ -171,22 +171,42 @@ const unsigned* block_order(po_tree* t, int W, int H, cudaStream_t s, cudaError_
     return d_ord;
 }
 
-// The level-(D-1) cell index (kOptGrid): for every cell of the 2^(D-1)-per-axis grid the entry
-// of the depth-(D-1) node covering it, a depth-(D-1) leaf's entry, or the level of the empty box
-// containing it (0xFFFFFFFF: a coarser leaf, traversed the classic way).  Built on the host from
-// the caller's child table inside po_tree_create (D in 2..10; 67 MB at D = 9, 537 MB at D = 10)
-// unless the descriptor sets PO_TREE_NO_INDEX; read-only afterwards, so renders stay
-// asynchronous and allocation-free.  Returns the CUDA error of the upload (cudaSuccess when D is
-// outside 2..10: every kernel then descends classically).
+// The level-(D-1) cell index (kOptGrid, traverse.cuh DevTree::grid): for every cell of the
+// 2^(D-1)-per-axis grid an (E, F) pair -- the level of the empty box containing it, a depth-(D-1)
+// leaf's entry, a depth-(D-1) node's child-table entry, or, when that node's leaves are numbered
+// consecutively in octant order (the depth-first numbering of gen/ and of the paper's trees), its
+// occupancy mask and first leaf so a leaf-level step needs no child-table load (E = 0xFFFFFFFF: a
+// coarser leaf, traversed the classic way).  Built on the host from the caller's child table
+// inside po_tree_create (D in 2..10; 134 MB at D = 9, 1.07 GB at D = 10) unless the descriptor
+// sets PO_TREE_NO_INDEX; read-only afterwards, so renders stay asynchronous and allocation-free.
+// Returns the CUDA error of the upload (cudaSuccess when D is outside 2..10: every kernel then
+// descends classically).
 static cudaError_t build_grid(po_tree* t) {
     const int D = t->desc.max_depth;
     if (t->d_grid || D < 2 || D > 10) return cudaSuccess;
     const int G2 = 1 << (D - 1);
-    std::vector<uint32_t> g((size_t)G2 * G2 * G2, 0u);
+    std::vector<uint2> g((size_t)G2 * G2 * G2, make_uint2(0u, 0u));
     auto fill = [&](int x0, int y0, int z0, int n, uint32_t v) {   // grid cells [x0, x0+n)^3
         for (int x = x0; x < x0 + n; ++x)
             for (int y = y0; y < y0 + n; ++y)
-                for (int z = z0; z < z0 + n; ++z) g[((size_t)x * G2 + y) * G2 + z] = v;
+                for (int z = z0; z < z0 + n; ++z) g[((size_t)x * G2 + y) * G2 + z] = make_uint2(v, 0u);
+    };
+    // a depth-(D-1) node: packed (mask, first leaf) when its leaves are consecutive in octant order
+    auto node_entry = [&](uint32_t e) -> uint2 {
+        const uint32_t node = e & ((1u << 30) - 1u);
+        uint32_t mask = 0u, first = 0u, rank = 0u;
+        bool packed = true;
+        for (int oct = 0; oct < 8; ++oct) {
+            const uint32_t c = t->h_child[(size_t)node * 8 + oct];
+            if ((c >> 30) == 0u) continue;
+            const uint32_t idx = c & ((1u << 30) - 1u);
+            if ((c >> 30) != 2u || (rank == 0 ? false : idx != first + rank)) packed = false;
+            if (rank == 0) first = idx;
+            mask |= 1u << oct;
+            ++rank;
+        }
+        if (packed && rank > 0) return make_uint2((3u << 30) | mask, first);
+        return make_uint2(e, 0u);
     };
     // node at `level` with its box corner in grid cells (level-(D-1) units), box edge 2^(D-1-level)
     std::function<void(uint32_t, int, int, int, int)> rec = [&](uint32_t node, int level, int x0, int y0, int z0) {
@@ -196,7 +216,7 @@ static cudaError_t build_grid(po_tree* t) {
             const int cx = x0 + ((oct >> 2) & 1) * half, cy = y0 + ((oct >> 1) & 1) * half, cz = z0 + (oct & 1) * half;
             const uint32_t tag = e >> 30;
             if (tag == 1u) {
-                if (level + 1 == D - 1) g[((size_t)cx * G2 + cy) * G2 + cz] = e;
+                if (level + 1 == D - 1) g[((size_t)cx * G2 + cy) * G2 + cz] = node_entry(e);
                 else rec(e & ((1u << 30) - 1u), level + 1, cx, cy, cz);
             } else if (tag == 2u) {
                 fill(cx, cy, cz, half, level + 1 == D - 1 ? e : 0xFFFFFFFFu);
@@ -206,19 +226,19 @@ static cudaError_t build_grid(po_tree* t) {
         }
     };
     rec(0u, 0, 0, 0, 0);
-    uint32_t* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, g.size() * 4);
+    uint2* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, g.size() * sizeof(uint2));
     if (e != cudaSuccess) {
         (void)cudaGetLastError();   // not sticky: po_tree_create reports it
         return e;
     }
-    if ((e = cudaMemcpy(d, g.data(), g.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
+    if ((e = cudaMemcpy(d, g.data(), g.size() * sizeof(uint2), cudaMemcpyHostToDevice)) != cudaSuccess) {
         (void)cudaGetLastError();
         cudaFree(d);
         return e;
     }
     t->d_grid = d;
-    t->grid_bytes = g.size() * 4;
+    t->grid_bytes = g.size() * sizeof(uint2);
     return cudaSuccess;
 }
 
@@ -406,7 +426,7 @@ po_status po_tree_create(const po_tree_desc* desc, const uint32_t* child, int64_
         if (e != cudaSuccess)
             return cleanup(fail(e == cudaErrorMemoryAllocation ? PO_ERR_OOM : PO_ERR_CUDA,
                                 "level-(D-1) cell index (%.0f MB): %s; PO_TREE_NO_INDEX creates the tree without it",
-                                std::ldexp(1.0, 3 * (D - 1)) * 4 / 1e6, cudaGetErrorString(e)));
+                                std::ldexp(1.0, 3 * (D - 1)) * 8 / 1e6, cudaGetErrorString(e)));
     }
     *out = t;
     return PO_OK;

@@ -41,9 +41,14 @@ struct DevTree {
     // NEXT f3, spherical Gaussians: B lobes (unit axis xyz, bandwidth) replacing
     // the SH basis when non-null (po_tree_set_sg_basis)
     const float4* __restrict__ sg;
-    // experiment kOptGrid: entry of every level-(D-1) cell (internal node / leaf / empty box
-    // level, 0xFFFFFFFF = fall back), 2^(D-1) per axis, x-major; null when not built
-    const uint32_t* __restrict__ grid = nullptr;
+    // kOptGrid cell index: one (E, F) pair per level-(D-1) cell, 2^(D-1) per axis, x-major;
+    // null when not built.  E = tag << 30 | payload:
+    //   tag 0: empty box, payload = its level          tag 2: a depth-(D-1) leaf (its entry)
+    //   tag 1: a depth-(D-1) node (child-table entry)  tag 3: a depth-(D-1) node whose leaves
+    //   are consecutive in octant order: payload = 8-bit occupancy mask, F = its first leaf, so
+    //   a leaf-level cell's entry is F + popc(mask below its octant) -- no child-table load
+    //   0xFFFFFFFF: a leaf coarser than D-1 covers the cell (classic descent)
+    const uint2* __restrict__ grid = nullptr;
 };
 
 struct RayState {
@@ -159,11 +164,16 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
         if (tr.grid != nullptr && D >= 1) {
             const int G2 = G >> 1;
             while (true) {
-                const uint32_t E = __ldg(tr.grid + (((size_t)(c[0] >> 1) * G2 + (c[1] >> 1)) * G2 + (c[2] >> 1)));
+                const uint2 EF = __ldg(tr.grid + (((size_t)(c[0] >> 1) * G2 + (c[1] >> 1)) * G2 + (c[2] >> 1)));
+                const uint32_t E = EF.x;
                 uint32_t e;
                 int shift;
                 if (E == 0xFFFFFFFFu) {
                     break;   // a coarse leaf: not indexed (never in the benchmark trees); classic path below
+                } else if ((E >> 30) == 3u) {   // packed depth-(D-1) node: the leaf entry without a load
+                    const uint32_t oct = (uint32_t)(((c[0] & 1) << 2) | ((c[1] & 1) << 1) | (c[2] & 1));
+                    e = ((E >> oct) & 1u) ? ((kTagLeaf << 30) | (EF.y + __popc(E & ((1u << oct) - 1u) & 0xFFu))) : 0u;
+                    shift = 0;
                 } else if ((E >> 30) == kTagInternal) {
                     e = __ldg(tr.child + ((E & kIdxMask) * 8u + (uint32_t)(((c[0] & 1) << 2) | ((c[1] & 1) << 1) | (c[2] & 1))));
                     shift = 0;

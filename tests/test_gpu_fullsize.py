@@ -51,6 +51,58 @@ def test_c3_fp16_full_frame_sampled(env, c3_tree):
     assert (ref["n_proc"] > 0).sum() > 300      # the sample really hits the scene (458 of 2048 in r01)
 
 
+def _sampled_frame_check(po, om, tree, t, cfg, n_pix, seed, payload_f16, min_hits):
+    """One bench-configuration frame of `tree`; the oracle on n_pix sampled pixels (>= 95 % of
+    them tie-free, reading Q27).
+    fp32 payload: tie-free pixels within 1e-4 (north star), every excluded one within its bound.
+    fp16 payload (reading Q29): (1) against the oracle on the dequantised values the GPU holds,
+    every pixel within 1e-4 + its Q27 error-propagation bound (the band of a tie-free ray: with
+    sigma up to 1536 on c3 the fp32 crossings move a long ray's optical depth by more than 1e-4);
+    (2) against the fp32 values, tie-free pixels within 2e-3 (north star)."""
+    cam, W, H = gen.config_camera(cfg)
+    img = po.po_render(tree, po.cams_tensor(cam), W, H, gamma=0.01).reshape(-1, 3).cpu().numpy()
+    rays = om.camera_rays(cam, W, H)
+    pick = rng(seed).choice(W * H, n_pix, replace=False)
+    sh = t.sh.astype(np.float16).astype(np.float32) if payload_f16 else None
+    ot = om.OracleTree(t, sh=sh)
+    ref = om.render(ot, rays[pick], gamma=0.01)
+    f, bound = om.tie_flags(ot, rays[pick], gamma=0.01, with_bound=True)
+    ok = f == 0
+    assert ok.mean() >= 0.95, ok.sum()
+    err = np.abs(img[pick] - ref["rgb"]).max(axis=1)
+    print(f"{cfg}: {ok.sum()} tie-free of {n_pix}; max err tie-free {err[ok].max():.2e}, all {err.max():.2e}; "
+          f"band of tie-free rays p50 {np.median(bound[ok]):.1e} max {bound[ok].max():.1e}")
+    assert np.all(err <= bound + 1e-4), np.flatnonzero(err > bound + 1e-4)[:5]
+    if not payload_f16:
+        assert err[ok].max() <= 1e-4, err[ok].max()
+    else:
+        del ot
+        ref32 = om.render(om.OracleTree(t), rays[pick], gamma=0.01)
+        assert np.abs(img[pick][ok] - ref32["rgb"][ok]).max() <= 2e-3
+    assert (ref["n_proc"] > 0).sum() >= min_hits
+    return ok
+
+
+def test_c1_thick_paper_scale_sampled(env):
+    """The thick c1 variant (shell sdf/h in (-8, +1), a tree of the paper's mean size,
+    P:669 "1.93 GB"): bench launch, 4096 sampled pixels against the oracle."""
+    po, om, torch = env
+    t = gen.scene_c1(thick=True)
+    tree = po.tree_from_gen(t)
+    _, nl, rb = tree.info()
+    assert nl * (rb + 4) > 1.2e9   # > 1.2 GB of leaf payload on the device
+    _sampled_frame_check(po, om, tree, t, "c1", 4096, 95, False, 1000)
+
+
+def test_c3_sh25_fp16_sampled(env):
+    """The c3 scene at SH-25 (l = 4, the paper's T&T setting P:587-588; fp16 rows of 75 halves,
+    padded to 80): bench launch, 2048 sampled pixels against the oracle on the dequantised values."""
+    po, om, torch = env
+    t = gen.scene_c3(sh_degree=4)
+    tree = po.tree_from_gen(t, payload=po.PO_F16)
+    _sampled_frame_check(po, om, tree, t, "c3", 2048, 96, True, 300)
+
+
 def test_c1_backward_ray_subset(env, c1_tree):
     """c1 tree (3.4 M leaves), gamma = 0, 4096 training rays: GPU gradients vs the oracle."""
     po, om, torch = env

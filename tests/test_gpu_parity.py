@@ -241,7 +241,7 @@ def test_c1_trace_bit_exact_production_traversal(env, c1_tree):
     fed to both sides (the GPU's fp32 camera rays)."""
     po, om, torch = env
     tree = po.tree_from_gen(c1_tree)
-    assert tree.index_bytes() == 4 * 256 ** 3
+    assert tree.index_bytes() == 8 * 256 ** 3
     cam, W, H = gen.config_camera("c1")
     rays = po.po_camera_rays(po.cams_tensor(cam), W, H).reshape(-1, 6)
     pick = torch.from_numpy(rng(18).choice(W * H, 8192, replace=False)).cuda()
