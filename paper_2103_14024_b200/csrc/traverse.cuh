@@ -16,9 +16,6 @@
 // (old XOR new) cell coordinates, from a per-thread ancestor stack.  Empty coarse boxes
 // are skipped in one step.
 #pragma once
-#ifndef PO_TE_FMA
-#define PO_TE_FMA 0   // A/B: plane crossings as one FFMA with a per-ray o * inv
-#endif
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -58,9 +55,6 @@ struct RayState {
     float o[3];     // origin in grid units
     float dg[3];    // unit direction * scale (grid units per world unit)
     float inv[3];   // 1 / dg (world t per grid unit), +inf for a zero component
-#if PO_TE_FMA
-    float oinv[3];  // o * inv: a plane crossing is one FFMA, fma(plane, inv, -oinv)
-#endif
     float d[3];     // unit world direction (SH argument, reading Q15)
     float tnear, tfar;
 };
@@ -91,18 +85,12 @@ __device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], c
         r.dg[k] = r.d[k] * tr.scale;
         if (r.dg[k] != 0.f) {
             r.inv[k] = 1.0f / r.dg[k];
-#if PO_TE_FMA
-            r.oinv[k] = r.o[k] * r.inv[k];
-#endif
             float ta = (0.f - r.o[k]) * r.inv[k];
             float tb = (G - r.o[k]) * r.inv[k];
             tn = fmaxf(tn, fminf(ta, tb));
             tf = fminf(tf, fmaxf(ta, tb));
         } else {
             r.inv[k] = INFINITY;
-#if PO_TE_FMA
-            r.oinv[k] = r.o[k] * INFINITY;   // +-inf or NaN: the crossing is NaN, which fminf ignores
-#endif
             if (!(r.o[k] >= 0.f && r.o[k] <= G)) return false;
         }
     }
@@ -114,11 +102,7 @@ __device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], c
 // world t at which the ray crosses the integer plane `face` of axis k (the same expression in
 // every kernel, so all of them walk identical boxes with identical t)
 __device__ __forceinline__ float plane_t(const RayState& r, int k, int face) {
-#if PO_TE_FMA
-    return fmaf((float)face, r.inv[k], -r.oinv[k]);
-#else
     return ((float)face - r.o[k]) * r.inv[k];
-#endif
 }
 
 // Cell index on one axis of the point o' + t*dg, for a ray moving with slope dg:

@@ -150,3 +150,36 @@ def test_sg_basis_render_and_backward(env, deg, gamma):
     assert torch.equal(sh_out, po.po_render_rays(po.tree_from_gen(t), r, gamma=gamma))
     with pytest.raises(po.PoError):
         tree.set_sg_basis(np.zeros((B, 3), np.float32), lam)
+
+
+def test_sg_tree_scratch_growth_keeps_lobes(env):
+    """Scratch growth must not touch the tree's other device buffers (round-1 advisor finding:
+    po_backward_plan's growth freed the deterministic scratch and the SG lobes): an SG tree runs
+    the deterministic backward, then po_backward_plan on a larger batch (its scratch grows), then
+    renders and backpropagates again -- identical to a fresh SG tree -- and is destroyed."""
+    po, om, torch = env
+    t = gen.scene_random(79, depth=5, sh_degree=2, sigma_scale=3.0)
+    axes, lam = _sg_lobes(9, 11)
+    tree = po.tree_from_gen(t)
+    tree.set_sg_basis(axes, lam)
+    fresh = po.tree_from_gen(t)
+    fresh.set_sg_basis(axes, lam)
+    rays = torch.from_numpy(gen.random_rays(80, 2000, inside_frac=0.1)).cuda()
+    n = rays.shape[0]
+    g = torch.randn((n, 3), device="cuda")
+    aux = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+    seg = po.Segments(n, 64)
+    po.po_render_rays(tree, rays, aux=aux, gamma=0.0, segments=seg)
+    gs = torch.zeros(tree.n_leaves, device="cuda")
+    gk = torch.zeros((tree.n_leaves, 9, 3), device="cuda")
+    po.po_render_backward_deterministic(tree, rays, g, gs, gk, aux, seg, gamma=0.0)
+    for m in (100, 50000):   # the plan scratch grows on the second call
+        span = torch.zeros((m, 2), dtype=torch.int32, device="cuda")
+        po.po_backward_plan(tree, span, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(po.po_render_rays(tree, rays, gamma=0.01), po.po_render_rays(fresh, rays, gamma=0.01))
+    gs2, gk2 = torch.zeros_like(gs), torch.zeros_like(gk)
+    po.po_render_backward_deterministic(tree, rays, g, gs2, gk2, aux, seg, gamma=0.0)
+    assert torch.equal(gs, gs2) and torch.equal(gk, gk2)
+    tree.destroy()
+    fresh.destroy()

@@ -14,6 +14,6 @@ for wl in "c1 --steps 20" "c1 --steps 20 --shard tile" "c2 --steps 5" "c4 --step
   echo "$wl 2-rank exit $?"; tail -1 gpurun_out/multirank_$1$3$4.log | cut -c1-240
   port=$((port + 1))
 done
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port $port \
-    tools/rs_vs_ar.py 2>&1 | grep -E "^rank"
-echo "reduce-scatter vs allreduce exit ${PIPESTATUS[0]}"
+
+
+# reduce-scatter vs allreduce (bitwise): tests/test_gpu_multirank.py

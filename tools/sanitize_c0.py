@@ -25,6 +25,7 @@ g = torch.randn((rays.shape[0], 3), device="cuda")
 po.po_render_backward(tree, rays, g, gs, gk, gamma=0.0)
 po.po_render_backward(tree, rays, g, gs, gk, aux=aux, gamma=0.0)
 po.po_trace(tree, rays, max_leaves=16)
+po.po_trace(tree, rays, max_leaves=16, classic=True)
 po.po_render_stats(tree, ct, W, H)
 opt = OctreeOptimizer(tree, lr=1.0)
 opt.step(rays, out)
