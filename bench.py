@@ -530,6 +530,9 @@ def run_c4(args):
     if rank == 0:
         peak, peak_src = _peaks()
         alg = (visits * (4 + 192 + 196) + nodes * 32) / K + n_rays * (24 + 12 + 32)
+        # per visited leaf 2 record reads + the 196-B gradient RMW (588 B), a node
+        # sector per internal node for each of the two traversals, rays/colours/targets
+        alg_survey = (visits * 588 + nodes * 64) / K + n_rays * (24 + 12 + 32)
         fused = (opt.fused_sgd and ws == 1 and not args.deterministic and args.max_seg > 0 and opt.n_chunks() == 1)
         line = {
             "metric": "direct octree optimisation rays/s (c4: forward+backward+allreduce+SGD)",
@@ -554,9 +557,16 @@ def run_c4(args):
             "loss_first_last": [float(losses[0].item()), float(losses[-1].item())],
             "leaf_visits_per_step": visits / K,
             "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
-                         "alg_bytes_per_step": round(alg),
+                         "alg_bytes_per_step": round(alg_survey),
+                         "achieved": round(alg_survey / (t_max / K / 1e3) / 1e9, 1),
+                         "frac": round(alg_survey / (t_max / K / 1e3) / 1e9 / peak, 4),
+                         "alg_bytes_def": "SURVEY 8(d): visits*588 B (pass-1 and pass-2 record reads + 196 B "
+                                          "gradient RMW) + nodes*2*32 B + rays*68 B",
+                         "alg_bytes_as_implemented": round(alg),
                          "achieved_step": round(alg / (t_max / K / 1e3) / 1e9, 1),
-                         "alg_bytes_def": "visits*(4 sigma + 192 SH row + 196 gradient RMW) + nodes*32 + rays*68"},
+                         "as_implemented_def": "visits*(4 sigma + 192 SH row + 196 gradient RMW) + nodes*32 + rays*68 "
+                                               "(pass 2 replays 32-B stored segment records instead of re-reading "
+                                               "the tree)"},
             "gpu_launches": int(launches), "clocks": clk,
             "e2e": {"value": round(e2e_value, 1), "unit": "rays/s", "h2d_bytes_per_step": n_rays * (24 + 12),
                     "d2h_bytes_per_step": 8, "entry": "OctreeOptimizer.train_from_host on pinned host batches (every step's "
@@ -658,8 +668,9 @@ def main():
                     help="c4: pass-2 chunks overlapped with the allreduce (default 4 if N>1, else 1)")
     ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
-    ap.add_argument("--ray-order", choices=["sampled", "leaf", "tileleaf"], default="leaf",
-                    help="c4: keep the sampled order or sort the batch by first-entered leaf")
+    ap.add_argument("--ray-order", choices=["sampled", "leaf", "tileleaf"], default="tileleaf",
+                    help="c4: keep the sampled order, sort the rays by first-entered leaf, or keep each 8x4 "
+                         "tile's rays together and sort the tiles by their lowest first-entered leaf")
     ap.add_argument("--ray-sampling", choices=["tile", "pixel"], default="tile",
                     help="c4: sample 8x4 pixel tiles (coherent warps) or single pixels")
     args = ap.parse_args()

@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(256, 3) k_backward_replay_sgd(DevTree tr, cons
 // whose warps stride over perm[chunk_end[c-1] .. chunk_end[c]) (static: ~100 rays per warp on
 // c4, balanced without a shared counter)
 template <int DEG>
-__global__ void __launch_bounds__(256, 3) k_backward_replay_chunk(DevTree tr, const float* __restrict__ rays,
+__global__ void __launch_bounds__(256, 2) k_backward_replay_chunk(DevTree tr, const float* __restrict__ rays,
                                                                const int32_t* __restrict__ perm,
                                                                const int64_t* __restrict__ chunk_end, int chunk,
                                                                const float* __restrict__ dL_dC,
