@@ -159,6 +159,11 @@ def _init_pg(dev_index: int):
         dist.init_process_group(backend)
 
 
+ORDER_DESC = ("16x16 blocks handed out costliest first by the per-block cost the previous single-view render "
+              "on the stream measured (temporal coherence of the orbit; the first render centre-out; images do "
+              "not depend on the order; DESIGN.md 6.1 v13)")
+
+
 def _workload_desc(tree_gen, wl="c1", ws=1):
     if wl == "c2":
         return {"workload": "c2: the c1 tree (depth-9, "
@@ -174,12 +179,14 @@ def _workload_desc(tree_gen, wl="c1", ws=1):
                             "1920x1080, gamma 0.01",
                 "views": "orbit r 2.6, el 15 deg, az = 20 + 1.8*i deg, f 1400 px; rank r renders views r, r+N, ...",
                 "l2": L2_DESC,
+                "block_order": ORDER_DESC,
                 "global_batch": "1 frame per rank per step"}
     thick = " thick shell sdf/h in (-8, +1) (SURVEY 8(d) paper-scale variant, P:669 mean 1.93 GB)," if wl == "c1thick" else ""
     return {"workload": f"{wl}: NeRF-synthetic-shaped SDF object, depth-9 sparse octree (512^3),{thick} "
                         f"{tree_gen.n_leaves} leaves / {tree_gen.n_nodes} nodes, SH-3 fp32 payload, 800x800, gamma 0.01",
             "views": "c1 orbit, az = 37 + 1.8*i deg, el 30 deg, r 3.4, f 1111.1 px; rank r renders views r, r+N, ...",
             "l2": L2_DESC,
+            "block_order": ORDER_DESC,
             "global_batch": "1 frame per rank per step"}
 
 

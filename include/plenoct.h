@@ -377,6 +377,11 @@ po_status po_render_timeline(const po_tree* tree, const po_camera* cams, int32_t
                              const po_render_opts* opts, float* out_rgb, unsigned long long* timeline,
                              po_stream stream);
 
+/* po_set_block_order: replaces the tree's block hand-out order for W x H renders by the host
+ * array order[ceil(W/16)*ceil(H/16)] (hand-out position -> block index in raster order; a
+ * permutation, checked).  Scheduling experiments only. */
+po_status po_set_block_order(po_tree* tree, int32_t W, int32_t H, const uint32_t* order);
+
 /* Number of kernel launches the library has issued since load (bench accounting). */
 int64_t po_launch_count(void);
 

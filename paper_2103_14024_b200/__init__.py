@@ -29,7 +29,7 @@ EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "
            "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
            "po_render_backward", "po_render_backward_sgd", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
-           "po_render_timeline", "po_ray_step_timing"]
+           "po_render_timeline", "po_ray_step_timing", "po_set_block_order"]
 
 
 class PoError(RuntimeError):
@@ -114,6 +114,7 @@ def lib():
         L.po_render_stats.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_timeline.argtypes = [P, P, I32, I32, I32, P, P, P, P]
         L.po_ray_step_timing.argtypes = [P, P, I64, P, I32, P, P, P]
+        L.po_set_block_order.argtypes = [P, I32, I32, P]
         for name in EXPORTS:
             if name not in ("po_last_error", "po_version", "po_launch_count"):
                 getattr(L, name).restype = ctypes.c_int
@@ -546,6 +547,12 @@ def po_render_timeline(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.
     _check(lib().po_render_timeline(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), _ptr(out), _ptr(tl),
                                     _stream(stream)))
     return out, tl
+
+
+def po_set_block_order(tree: PlenOctree, W: int, H: int, order):
+    """Diagnostics: replace the block hand-out order of W x H renders (include/plenoct.h)."""
+    order = np.ascontiguousarray(order, dtype=np.uint32)
+    _check(lib().po_set_block_order(tree.handle, W, H, _ptr(order)))
 
 
 def po_ray_step_timing(tree: PlenOctree, rays, max_steps: int = 1024, gamma: float = 0.01, stream=None):

@@ -72,6 +72,14 @@ struct po_tree {
         return i < 0 ? nullptr : d_work + kWorkStride * i;
     }
     int* sgd_flag() { return reinterpret_cast<int*>(d_work + kWorkStride * kWorkSlots); }
+    // cost-ordered hand-out of single-view renders (DESIGN.md §6.1 v13): per work slot (stream)
+    // a device table [n_blocks] order + [n_blocks] per-block cost for one W x H, rewritten by
+    // every single-view render on that stream for the next one
+    struct StreamOrder {
+        unsigned* d = nullptr;
+        int W = 0, H = 0;
+    };
+    std::vector<StreamOrder> stream_order;   // indexed like work_streams, under work_mu
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
     uint2* d_grid = nullptr;         // dense level-(D-1) cell index (build_grid, at po_tree_create)
     size_t grid_bytes = 0;
@@ -543,6 +551,8 @@ po_status po_tree_destroy(po_tree* t) {
     if (t->pipe_stream) cudaStreamDestroy(t->pipe_stream);
     if (t->d_order) cudaFree(t->d_order);
     if (t->d_order_zip) cudaFree(t->d_order_zip);
+    for (auto& so : t->stream_order)
+        if (so.d) cudaFree(so.d);
     if (t->d_grid) cudaFree(t->d_grid);
     if (t->d_plan) cudaFree(t->d_plan);
     if (t->d_det) cudaFree(t->d_det);
@@ -612,17 +622,66 @@ static po_status check_cams_host(const po_camera* c, int32_t n) {
     return PO_OK;
 }
 
-// Block hand-out order (centre-out, block_order) and launch of the persistent render kernel.
-// (An order by measured or probed block cost was tried in r01 and was slower: DESIGN.md §6.1.)
+// The stream's cost-ordered table for single-view W x H renders (order + cost, 2 x n_blocks
+// uint32), set up on first use or a size change: the centre-out order and zero costs, copied on
+// the stream (no host sync except when an old table of another size is freed).
+static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, const unsigned* centre, cudaError_t* err) {
+    *err = cudaSuccess;
+    const size_t nb = (size_t)((W + 15) / 16) * ((H + 15) / 16);
+    std::lock_guard<std::mutex> lk(t->work_mu);
+    const int slot = t->slot_of(s);
+    if (slot < 0) return nullptr;
+    if ((int)t->stream_order.size() <= slot) t->stream_order.resize(slot + 1);
+    po_tree::StreamOrder& so = t->stream_order[slot];
+    if (so.d && so.W == W && so.H == H) return so.d;
+    if (so.d) {
+        if ((*err = cudaStreamSynchronize(s)) != cudaSuccess) return nullptr;   // the old table may be in use
+        cudaFree(so.d);
+        so.d = nullptr;
+    }
+    if ((*err = cudaMalloc(&so.d, 2 * nb * sizeof(unsigned))) != cudaSuccess) {
+        so.d = nullptr;
+        return nullptr;
+    }
+    if ((*err = cudaMemcpyAsync(so.d, centre, nb * sizeof(unsigned), cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
+        (*err = cudaMemsetAsync(so.d + nb, 0, nb * sizeof(unsigned), s)) != cudaSuccess) {
+        cudaFree(so.d);
+        so.d = nullptr;
+        return nullptr;
+    }
+    so.W = W;
+    so.H = H;
+    return so.d;
+}
+
+// Block hand-out order and launch of the persistent render kernel.  Single-view renders hand
+// blocks out costliest first by the costs the previous single-view render of the same size on
+// the same stream measured (temporal coherence of a moving camera; the first one uses the
+// centre-out order); other launches use the centre-out order (DESIGN.md §6.1 v13).
+// PO_RENDER_ORDER=centre keeps the centre-out order for every launch, =raster raster order.
 static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams, int W, int H,
                                   const po::RenderOpts& o, float* out, cudaStream_t s, const char* where,
                                   unsigned long long* timeline = nullptr, bool zip = false, bool raster = false) {
+    static const bool centre_only = [] {
+        const char* e = getenv("PO_RENDER_ORDER");
+        return e && (std::strcmp(e, "centre") == 0 || std::strcmp(e, "raster") == 0);
+    }();
     cudaError_t e = cudaSuccess;
     const unsigned* order = raster ? nullptr : block_order(t, W, H, s, &e, zip);
     if (e != cudaSuccess) return cuda_status(e, "block order");
     unsigned* work = t->work_for(s);
     if (!work) return fail(PO_ERR_UNSUPPORTED, "%s: more than %d distinct streams on one tree", where, po_tree::kWorkSlots);
-    return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o,
+    po::RenderOpts o2 = o;
+    const size_t nb = (size_t)((W + 15) / 16) * ((H + 15) / 16);
+    if (order != nullptr && !zip && !centre_only && n_cams == 1 && o.shard_count == 1 && nb <= 16384) {
+        unsigned* tab = stream_order_table(t, s, W, H, order, &e);
+        if (e != cudaSuccess) return cuda_status(e, "stream block order");
+        if (tab) {
+            order = tab;
+            o2.blk_cost = tab + nb;
+        }
+    }
+    return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o2,
                                       out, work, order, timeline, s),
                     where);
 }
@@ -1266,6 +1325,34 @@ po_status po_render_timeline(const po_tree* t, const po_camera* cams, int32_t n_
     if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
     return render_scheduled(const_cast<po_tree*>(t), cams, n_cams, W, H, o, out_rgb, (cudaStream_t)stream,
                             "po_render_timeline", timeline);
+#endif
+}
+
+po_status po_set_block_order(po_tree* t, int32_t W, int32_t H, const uint32_t* order) {
+#ifndef PO_DIAG
+    (void)t, (void)W, (void)H, (void)order;
+    return fail(PO_ERR_UNSUPPORTED, "%s: diagnostics are built only with -DPO_DIAG", "po_set_block_order");
+#else
+    if (po_status s = check_tree(t)) return s;
+    if (po_status s = check_image(1, W, H)) return s;
+    if (!order) return fail(PO_ERR_INVALID_ARG, "NULL order");
+    const size_t nb = (size_t)((W + 15) / 16) * ((H + 15) / 16);
+    std::vector<char> seen(nb, 0);
+    for (size_t i = 0; i < nb; ++i) {
+        if (order[i] >= nb || seen[order[i]]) return fail(PO_ERR_INVALID_ARG, "order is not a permutation");
+        seen[order[i]] = 1;
+    }
+    DeviceGuard g(t->desc.device);
+    if (g.err != cudaSuccess) return cuda_status(g.err, "cudaSetDevice");
+    cudaError_t e = cudaSuccess;
+    block_order(t, W, H, nullptr, &e);   // allocates the table for this size
+    if (e != cudaSuccess) return cuda_status(e, "block order");
+    std::lock_guard<std::mutex> lk(t->order_mu);
+    if (!t->d_order) return fail(PO_ERR_UNSUPPORTED, "raster order (PO_RENDER_ORDER=raster)");
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_status(e, "sync");
+    if ((e = cudaMemcpy(t->d_order, order, nb * sizeof(unsigned), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_status(e, "order copy");
+    return PO_OK;
 #endif
 }
 

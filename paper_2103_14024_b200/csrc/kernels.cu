@@ -334,6 +334,52 @@ __device__ __forceinline__ bool tile_pixel(int W, int H, int& px, int& py) {
 // across SMs with no tail wave.  The last CTA to finish resets the global counters
 // (work[0] = next block, work[1] = finished CTAs) for the next launch on the stream.
 constexpr int kSlotRing = 16;
+
+// Cost-ordered hand-out (DESIGN.md §6.1 v13).  A frame ends with its slowest warp tiles (grazing
+// rays along the surface shell); handing their blocks out first makes them start at t = 0
+// instead of in the second wave.  Consecutive frames of a moving camera have nearly the same
+// per-block costs, so each single-view launch measures them (max SM cycles of a block's warp
+// tiles) and its last CTA rewrites the stream's order table for the next launch: a counting
+// sort over 256 log2-spaced cost buckets (2^(1/8) apart), costliest first.  Pixel values do not
+// depend on the order.  key8 = shared scratch of >= nb bytes.
+__device__ __forceinline__ void reorder_blocks(unsigned* __restrict__ cost, unsigned* __restrict__ order, unsigned nb,
+                                               uint8_t* __restrict__ key8) {
+    __shared__ unsigned hist[256];
+    const unsigned tid = threadIdx.x;
+    for (unsigned i = tid; i < 256u; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    for (unsigned i = tid; i < nb; i += blockDim.x) {
+        const unsigned c = atomicExch(cost + i, 0u);   // read and reset for the next launch
+        const int lg = c == 0u ? 0 : min(255, (int)(8.f * __log2f((float)c)));
+        const unsigned k = 255u - (unsigned)lg;         // costliest -> bucket 0
+        key8[i] = (uint8_t)k;
+        atomicAdd(&hist[k], 1u);
+    }
+    __syncthreads();
+    if (tid < 32u) {   // exclusive scan of the 256 buckets, 8 per lane
+        unsigned v[8], sum = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = hist[tid * 8u + j];
+            sum += v[j];
+        }
+        unsigned x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if ((int)tid >= o) x += y;
+        }
+        unsigned base = x - sum;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            hist[tid * 8u + j] = base;
+            base += v[j];
+        }
+    }
+    __syncthreads();
+    for (unsigned i = tid; i < nb; i += blockDim.x) order[atomicAdd(&hist[key8[i]], 1u)] = i;
+}
+
 template <int DEG, bool F16, int MINB, int OPT>
 __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camera* __restrict__ cams, int n_cams, int W,
                                                 int H, RenderOpts opt, float* __restrict__ out,
@@ -386,6 +432,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         if (order != nullptr) rem = __ldg(order + rem);   // block hand-out order (see launch_render)
         unsigned long long t_tile = 0;
         if (timeline != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_tile));
+        const unsigned c_tile = opt.blk_cost != nullptr ? (unsigned)clock() : 0u;
         const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
         const int px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
         const int py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
@@ -430,6 +477,10 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
             }
         }
         store_tile_rgb(out, (size_t)view * H, W, H, bx * 16 + (int)(sub & 1u) * 8, by * 16 + (int)(sub >> 1) * 4, C);
+        if (opt.blk_cost != nullptr) {   // this tile's cost (SM cycles) for the next launch's order
+            __syncwarp();
+            if (lane == 0) atomicMax(opt.blk_cost + rem, (unsigned)clock() - c_tile);
+        }
         if (opt.band_done != nullptr) {   // this tile's pixels are stored: count it for its band
             __threadfence();
             __syncwarp();
@@ -452,11 +503,21 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         }
     }
     __syncthreads();
+    __shared__ unsigned s_last;
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+        const bool last = atomicAdd(work + 1, 1u) == gridDim.x - 1;
+        if (last) {
             atomicExch(work, 0u);
             atomicExch(work + 1, 0u);
+        }
+        s_last = last ? 1u : 0u;
+    }
+    if (opt.blk_cost != nullptr) {
+        __syncthreads();
+        if (s_last) {   // every other CTA has finished: build the next launch's order
+            __threadfence();
+            reorder_blocks(opt.blk_cost, const_cast<unsigned*>(order), per_view, reinterpret_cast<uint8_t*>(stk_storage));
         }
     }
 }

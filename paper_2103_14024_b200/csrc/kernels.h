@@ -21,6 +21,11 @@ struct RenderOpts {
     // band_done[block_row / band_rows] (cumulative 64-bit counters a copy stream waits on)
     unsigned long long* band_done = nullptr;
     int32_t band_rows = 0;
+    // k_render only, single-view launches (cost-ordered hand-out, DESIGN.md §6.1 v13): non-null
+    // = device uint32[n_blocks] per-block cost (max SM cycles of its warp tiles), zero on entry;
+    // the last CTA then rewrites `order` (costliest block first) for the next launch on the
+    // stream and zeroes the costs again.  `order` must then be a mutable per-stream table.
+    unsigned* blk_cost = nullptr;
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.

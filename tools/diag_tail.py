@@ -31,6 +31,16 @@ dur = t1 - t0
 blk = rec[:, 2] & 0xFFFFFFFF
 sub = idx % 8
 print(f"frame span {t1.max():.1f} us, {len(dur)} tiles")
+pos = idx // 8   # hand-out position of the tile's block (centre-out order)
+for q in (50, 90, 99, 99.9):
+    print(f"  tile duration p{q}: {np.percentile(dur, q):.1f} us")
+for thr in (100, 120, 140, 160):
+    sel = t1 > thr
+    print(f"  tiles ending after {thr} us: {int(sel.sum())}, their hand-out positions p50 {np.median(pos[sel]) if sel.any() else -1:.0f} max {pos[sel].max() if sel.any() else -1}")
+top30 = np.argsort(-t1)[:30]
+print("  last 30 tiles to finish (hand-out pos, start, dur):", [(int(pos[j]), round(float(t0[j]), 1), round(float(dur[j]), 1)) for j in top30])
+topd = np.argsort(-dur)[:30]
+print("  30 longest tiles (hand-out pos, start, dur):", [(int(pos[j]), round(float(t0[j]), 1), round(float(dur[j]), 1)) for j in topd])
 rays_all = po.po_camera_rays(cams[6:7], 800, 800).reshape(800, 800, 6)
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 top = np.argsort(-dur)[:12]
@@ -93,3 +103,6 @@ k = int(torch.argmax(nodes0).item())
 print(f"slowest ray x32 (identical lanes): {alone(tiles[0][k:k + 1].repeat(32, 1).contiguous()):.1f} us")
 for m in (1, 2, 4, 8, 16):
     print(f"slowest tile, first {m} lanes: {alone(tiles[0][:m].contiguous()):.1f} us")
+for j in range(4):   # each of the 4 slowest tiles as two 8x2 halves (16 lanes each)
+    print(f"tile {j}: 32 lanes {alone(tiles[j]):.1f} us, rows 0-1 {alone(tiles[j][:16].contiguous()):.1f} us, "
+          f"rows 2-3 {alone(tiles[j][16:].contiguous()):.1f} us")
