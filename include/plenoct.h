@@ -370,9 +370,10 @@ po_status po_render_stats(const po_tree* tree, const po_camera* cams, int32_t n_
 po_status po_ray_step_timing(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
                              int32_t max_steps, uint32_t* rec, int32_t* steps, po_stream stream);
 
-/* po_render_timeline: po_render that also records, for every 8x4-pixel warp tile, device
- * uint64 timeline[ceil(W/16)*ceil(H/16)*n_cams*8][4] = {globaltimer ns at tile start, at tile
- * end, SM id << 32 | block index in its view, view} (scheduling analysis; same image). */
+/* po_render_timeline: po_render that also records, for every warp tile, device uint64
+ * timeline[(ceil(W/16)*ceil(H/16)*n_cams + 192)*8][4] (record = hand-out position * 8 + tile)
+ * = {globaltimer ns at tile start, at tile end, SM id << 32 | block index in its view,
+ * view | split << 32 (0, or 8 | sub-block of a split block)} (scheduling analysis; same image). */
 po_status po_render_timeline(const po_tree* tree, const po_camera* cams, int32_t n_cams, int32_t W, int32_t H,
                              const po_render_opts* opts, float* out_rgb, unsigned long long* timeline,
                              po_stream stream);

@@ -542,7 +542,8 @@ def po_render_timeline(tree: PlenOctree, cams, W: int, H: int, gamma: float = 0.
     cams = _need(cams, torch.float32, (16,))
     n = cams.shape[0]
     out = torch.empty((n, H, W, 3), dtype=torch.float32, device=cams.device)
-    tl = torch.zeros((((W + 15) // 16) * ((H + 15) // 16) * n * 8, 4), dtype=torch.int64, device=cams.device)
+    # one record per warp tile and hand-out position (split blocks take up to 192 extra positions)
+    tl = torch.zeros(((((W + 15) // 16) * ((H + 15) // 16) * n + 192) * 8, 4), dtype=torch.int64, device=cams.device)
     o = _opts(gamma, background)
     _check(lib().po_render_timeline(tree.handle, _ptr(cams), n, W, H, ctypes.byref(o), _ptr(out), _ptr(tl),
                                     _stream(stream)))

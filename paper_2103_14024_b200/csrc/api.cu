@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <utility>
 #include <atomic>
 #include <cstdarg>
 #include <cstdlib>
@@ -622,12 +623,16 @@ static po_status check_cams_host(const po_camera* c, int32_t n) {
     return PO_OK;
 }
 
-// The stream's cost-ordered table for single-view W x H renders (order + cost, 2 x n_blocks
-// uint32), set up on first use or a size change: the centre-out order and zero costs, copied on
-// the stream (no host sync except when an old table of another size is freed).
+// The stream's cost-ordered table for single-view W x H renders, uint32: [0] = number of
+// hand-out positions, [1, 1 + nb + kSplitExtra) = order (split blocks expanded), then nb costs.
+// Set up on first use or a size change with the centre-out order and zero costs, copied on the
+// stream (no host sync except when an old table of another size is freed).
+constexpr int kSplitMaxK = 64, kSplitMaxF = 4;
+constexpr size_t kSplitExtra = (size_t)kSplitMaxK * (kSplitMaxF - 1);
 static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, const unsigned* centre, cudaError_t* err) {
     *err = cudaSuccess;
     const size_t nb = (size_t)((W + 15) / 16) * ((H + 15) / 16);
+    const unsigned n_pos = (unsigned)nb;
     std::lock_guard<std::mutex> lk(t->work_mu);
     const int slot = t->slot_of(s);
     if (slot < 0) return nullptr;
@@ -639,12 +644,14 @@ static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, co
         cudaFree(so.d);
         so.d = nullptr;
     }
-    if ((*err = cudaMalloc(&so.d, 2 * nb * sizeof(unsigned))) != cudaSuccess) {
+    if ((*err = cudaMalloc(&so.d, (1 + 2 * nb + kSplitExtra) * sizeof(unsigned))) != cudaSuccess) {
         so.d = nullptr;
         return nullptr;
     }
-    if ((*err = cudaMemcpyAsync(so.d, centre, nb * sizeof(unsigned), cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
-        (*err = cudaMemsetAsync(so.d + nb, 0, nb * sizeof(unsigned), s)) != cudaSuccess) {
+    // (a pageable source is staged before cudaMemcpyAsync returns)
+    if ((*err = cudaMemcpyAsync(so.d, &n_pos, sizeof(unsigned), cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (*err = cudaMemcpyAsync(so.d + 1, centre, nb * sizeof(unsigned), cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
+        (*err = cudaMemsetAsync(so.d + 1 + nb + kSplitExtra, 0, nb * sizeof(unsigned), s)) != cudaSuccess) {
         cudaFree(so.d);
         so.d = nullptr;
         return nullptr;
@@ -652,6 +659,22 @@ static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, co
     so.W = W;
     so.H = H;
     return so.d;
+}
+
+// (split_k, split_f) of cost-ordered renders: the costliest blocks rendered with fewer lanes per
+// warp tile (DESIGN.md §6.1 v14); PO_SPLIT_K / PO_SPLIT_F override it in diagnostics builds.
+static std::pair<int, int> split_cfg() {
+    static const std::pair<int, int> cfg = [] {
+        int k = 8, f = 2;
+#ifdef PO_DIAG
+        if (const char* e = getenv("PO_SPLIT_K")) k = atoi(e);
+        if (const char* e = getenv("PO_SPLIT_F")) f = atoi(e);
+#endif
+        k = k < 0 ? 0 : (k > kSplitMaxK ? kSplitMaxK : k);
+        if (f != 1 && f != 2 && f != 4) f = 1;
+        return std::make_pair(f == 1 ? 0 : k, f);
+    }();
+    return cfg;
 }
 
 // Block hand-out order and launch of the persistent render kernel.  Single-view renders hand
@@ -677,8 +700,10 @@ static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams,
         unsigned* tab = stream_order_table(t, s, W, H, order, &e);
         if (e != cudaSuccess) return cuda_status(e, "stream block order");
         if (tab) {
-            order = tab;
-            o2.blk_cost = tab + nb;
+            order = tab + 1;
+            o2.blk_cost = tab + 1 + nb + kSplitExtra;
+            o2.split_k = split_cfg().first;
+            o2.split_f = split_cfg().second;
         }
     }
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o2,

@@ -342,9 +342,14 @@ constexpr int kSlotRing = 16;
 // tiles) and its last CTA rewrites the stream's order table for the next launch: a counting
 // sort over 256 log2-spaced cost buckets (2^(1/8) apart), costliest first.  Pixel values do not
 // depend on the order.  key8 = shared scratch of >= nb bytes.
+// With split_k > 0 the split_k costliest blocks are expanded into split_f positions each
+// (entry = block | (8 | sub-block) << 28), placed first; order[-1] = number of positions.
 __device__ __forceinline__ void reorder_blocks(unsigned* __restrict__ cost, unsigned* __restrict__ order, unsigned nb,
-                                               uint8_t* __restrict__ key8) {
+                                               uint8_t* __restrict__ key8, int split_k, int split_f) {
     __shared__ unsigned hist[256];
+    __shared__ unsigned top[64];
+    const unsigned K = (split_f > 1) ? min((unsigned)split_k, min(nb, 64u)) : 0u;
+    const unsigned extra = K * (unsigned)(split_f - 1);
     const unsigned tid = threadIdx.x;
     for (unsigned i = tid; i < 256u; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
@@ -377,7 +382,15 @@ __device__ __forceinline__ void reorder_blocks(unsigned* __restrict__ cost, unsi
         }
     }
     __syncthreads();
-    for (unsigned i = tid; i < nb; i += blockDim.x) order[atomicAdd(&hist[key8[i]], 1u)] = i;
+    for (unsigned i = tid; i < nb; i += blockDim.x) order[extra + atomicAdd(&hist[key8[i]], 1u)] = i;
+    if (K > 0u) {
+        __syncthreads();
+        if (tid < K) top[tid] = order[extra + tid];
+        __syncthreads();
+        for (unsigned i = tid; i < K * (unsigned)split_f; i += blockDim.x)
+            order[i] = top[i / (unsigned)split_f] | ((8u | (i % (unsigned)split_f)) << 28);
+    }
+    if (tid == 0) order[-1] = nb + extra;
 }
 
 template <int DEG, bool F16, int MINB, int OPT>
@@ -398,7 +411,9 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
     // blocks of this shard per view: hand-out positions k = local * shard_count + shard_index
     const unsigned sc = (unsigned)opt.shard_count, si = (unsigned)opt.shard_index;
     const unsigned local_per_view = (per_view + sc - 1u - si) / sc;
-    const unsigned total = local_per_view * (unsigned)n_cams;
+    // cost-ordered single-view launches: order[-1] = hand-out positions (split blocks count
+    // split_f times, reorder_blocks); otherwise blocks of this shard x views
+    const unsigned total = opt.blk_cost != nullptr ? __ldg(order - 1) : local_per_view * (unsigned)n_cams;
     while (true) {
         // hand-off through shared-memory atomics (ordered by the block fences): the warp that
         // opens a slot claims the block and publishes it; the other 7 wait for the flag.  The
@@ -427,17 +442,28 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         if (lane == 0) blk = atomicAdd(&s_block[slot % kSlotRing], 0u);
         blk = __shfl_sync(0xffffffffu, blk, 0);
         if (blk >= total) break;
-        const unsigned view = blk / local_per_view;
-        unsigned rem = (blk - view * local_per_view) * sc + si;   // hand-out position in the view
+        const unsigned view = opt.blk_cost != nullptr ? 0u : blk / local_per_view;
+        unsigned rem = opt.blk_cost != nullptr ? blk : (blk - view * local_per_view) * sc + si;   // hand-out position
         if (order != nullptr) rem = __ldg(order + rem);   // block hand-out order (see launch_render)
+        const unsigned split = rem >> 28;                 // 0, or 8 | sub-block of a split block
+        rem &= 0x0FFFFFFFu;
         unsigned long long t_tile = 0;
         if (timeline != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_tile));
         const unsigned c_tile = opt.blk_cost != nullptr ? (unsigned)clock() : 0u;
         const int by = (int)(rem / bx_n), bx = (int)(rem - (unsigned)by * bx_n);
-        const int px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
-        const int py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
+        int px, py;
+        bool act = true;
+        if (split == 0u) {   // 8x4-pixel warp tile
+            px = bx * 16 + (int)(sub & 1u) * 8 + (lane & 7);
+            py = by * 16 + (int)(sub >> 1) * 4 + (lane >> 3);
+        } else {             // 4 x (8/F) pixels, lanes < 32/F (sub-block q of 16 x 16/F pixels)
+            const int F = opt.split_f, q = (int)(split & 7u);
+            px = bx * 16 + (int)(sub & 3u) * 4 + (lane & 3);
+            py = by * 16 + q * (16 / F) + (int)(sub >> 2) * (8 / F) + (lane >> 2);
+            act = lane < 32 / F;
+        }
         float C[3] = {opt.bg[0], opt.bg[1], opt.bg[2]};
-        if (px < W && py < H) {
+        if (act && px < W && py < H) {
             float o[3], d[3];
             if (opt.cam_inline) {   // single view passed by value (po_render_host): no H2D copy
                 float c[16];
@@ -476,10 +502,18 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                 }
             }
         }
-        store_tile_rgb(out, (size_t)view * H, W, H, bx * 16 + (int)(sub & 1u) * 8, by * 16 + (int)(sub >> 1) * 4, C);
+        if (split == 0u) {
+            store_tile_rgb(out, (size_t)view * H, W, H, bx * 16 + (int)(sub & 1u) * 8, by * 16 + (int)(sub >> 1) * 4, C);
+        } else if (act && px < W && py < H) {
+            float* p = out + ((size_t)py * W + px) * 3;
+            p[0] = C[0];
+            p[1] = C[1];
+            p[2] = C[2];
+        }
         if (opt.blk_cost != nullptr) {   // this tile's cost (SM cycles) for the next launch's order
             __syncwarp();
-            if (lane == 0) atomicMax(opt.blk_cost + rem, (unsigned)clock() - c_tile);
+            // a split block's tiles have 1/F of the rays: scaled so it keeps its rank
+            if (lane == 0) atomicMax(opt.blk_cost + rem, ((unsigned)clock() - c_tile) * (split ? (unsigned)opt.split_f : 1u));
         }
         if (opt.band_done != nullptr) {   // this tile's pixels are stored: count it for its band
             __threadfence();
@@ -498,7 +532,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                 rec[0] = t_tile;
                 rec[1] = t1;
                 rec[2] = (sm << 32) | rem;
-                rec[3] = view;
+                rec[3] = view | ((unsigned long long)split << 32);
             }
         }
     }
@@ -517,7 +551,8 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         __syncthreads();
         if (s_last) {   // every other CTA has finished: build the next launch's order
             __threadfence();
-            reorder_blocks(opt.blk_cost, const_cast<unsigned*>(order), per_view, reinterpret_cast<uint8_t*>(stk_storage));
+            reorder_blocks(opt.blk_cost, const_cast<unsigned*>(order), per_view, reinterpret_cast<uint8_t*>(stk_storage),
+                           opt.split_k, opt.split_f);
         }
     }
 }

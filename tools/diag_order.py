@@ -79,7 +79,7 @@ def dilate(c):
     return m.ravel()
 
 
-for v in range(6, 10):
+for v in (range(6, 10) if __name__ == "__main__" else ()):
     cm, cs = cost_of(v)
     pm, ps = cost_of(v - 1)
     r = {"centre": timed(v, centre), "own_max": timed(v, by_cost(cm)), "own_sum": timed(v, by_cost(cs)),
