@@ -46,4 +46,7 @@ for tool in memcheck racecheck synccheck initcheck; do
   echo "$tool $?"; tail -1 $O/$tool.log
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/l2bw tools/micro/l2bw.cu && for mb in 32 48 64 96; do /tmp/l2bw $mb 20; done > $O/l2bw.jsonl
+(export PO_NVCC_EXTRA=-DPO_DIAG; python -c 'from paper_2103_14024_b200 import _build; _build.build()' > $O/build_diag.log 2>&1 && \
+  timeout 600 python tools/diag_tail.py > $O/diag_tail.txt 2>&1; timeout 600 python tools/timeline_c1.py > $O/timeline_c1.txt 2>&1; echo "diag $?")
+python -c 'from paper_2103_14024_b200 import _build; _build.build()' > /dev/null 2>&1
 timeout 1800 python tools/oracle_baselines.py > $O/oracle_baselines.log 2>&1; echo "oracle baselines exit $?"; tail -1 $O/oracle_baselines.log | cut -c1-200

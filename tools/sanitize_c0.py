@@ -15,6 +15,9 @@ tree = po.tree_from_gen(t)
 cam, W, H = gen.config_camera("c0")
 ct = po.cams_tensor(cam)
 img = po.po_render(tree, ct, W, H)
+for _ in range(3):   # cost-ordered hand-out: order rewrite by the last CTA, split blocks (nb = 16)
+    po.po_render(tree, ct, W, H)
+po.po_render(tree, ct, 40, 24)   # stream order table re-initialised for another size
 rays = po.po_camera_rays(ct, W, H).reshape(-1, 6)
 out = po.po_render_rays(tree, rays)
 aux = torch.empty((rays.shape[0], 4), dtype=torch.float64, device="cuda")
