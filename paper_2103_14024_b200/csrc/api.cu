@@ -645,6 +645,7 @@ static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, co
         so.d = nullptr;
     }
     if ((*err = cudaMalloc(&so.d, (1 + 2 * nb + kSplitExtra) * sizeof(unsigned))) != cudaSuccess) {
+        (void)cudaGetLastError();   // reported by the caller, not left for the next launch check
         so.d = nullptr;
         return nullptr;
     }
@@ -652,6 +653,7 @@ static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, co
     if ((*err = cudaMemcpyAsync(so.d, &n_pos, sizeof(unsigned), cudaMemcpyHostToDevice, s)) != cudaSuccess ||
         (*err = cudaMemcpyAsync(so.d + 1, centre, nb * sizeof(unsigned), cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
         (*err = cudaMemsetAsync(so.d + 1 + nb + kSplitExtra, 0, nb * sizeof(unsigned), s)) != cudaSuccess) {
+        (void)cudaGetLastError();
         cudaFree(so.d);
         so.d = nullptr;
         return nullptr;
@@ -696,7 +698,7 @@ static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams,
     if (!work) return fail(PO_ERR_UNSUPPORTED, "%s: more than %d distinct streams on one tree", where, po_tree::kWorkSlots);
     po::RenderOpts o2 = o;
     const size_t nb = (size_t)((W + 15) / 16) * ((H + 15) / 16);
-    if (order != nullptr && !zip && !centre_only && n_cams == 1 && o.shard_count == 1 && nb <= 16384) {
+    if (order != nullptr && !centre_only && n_cams == 1 && o.shard_count == 1 && nb <= 16384) {
         unsigned* tab = stream_order_table(t, s, W, H, order, &e);
         if (e != cudaSuccess) return cuda_status(e, "stream block order");
         if (tab) {
@@ -704,6 +706,7 @@ static po_status render_scheduled(po_tree* t, const po_camera* cams, int n_cams,
             o2.blk_cost = tab + 1 + nb + kSplitExtra;
             o2.split_k = split_cfg().first;
             o2.split_f = split_cfg().second;
+            o2.zip_order = zip ? 1 : 0;
         }
     }
     return launched(po::launch_render(dev_tree(t), t->desc.sh_degree, t->desc.payload == PO_F16, cams, n_cams, W, H, o2,

@@ -344,8 +344,9 @@ constexpr int kSlotRing = 16;
 // depend on the order.  key8 = shared scratch of >= nb bytes.
 // With split_k > 0 the split_k costliest blocks are expanded into split_f positions each
 // (entry = block | (8 | sub-block) << 28), placed first; order[-1] = number of positions.
+// With zip the blocks after the split ones alternate costliest / cheapest (po_render_host).
 __device__ __forceinline__ void reorder_blocks(unsigned* __restrict__ cost, unsigned* __restrict__ order, unsigned nb,
-                                               uint8_t* __restrict__ key8, int split_k, int split_f) {
+                                               uint8_t* __restrict__ key8, int split_k, int split_f, bool zip) {
     __shared__ unsigned hist[256];
     __shared__ unsigned top[64];
     const unsigned K = (split_f > 1) ? min((unsigned)split_k, min(nb, 64u)) : 0u;
@@ -382,7 +383,15 @@ __device__ __forceinline__ void reorder_blocks(unsigned* __restrict__ cost, unsi
         }
     }
     __syncthreads();
-    for (unsigned i = tid; i < nb; i += blockDim.x) order[extra + atomicAdd(&hist[key8[i]], 1u)] = i;
+    const unsigned n2 = nb - K;   // blocks after the split ones
+    for (unsigned i = tid; i < nb; i += blockDim.x) {
+        unsigned r = atomicAdd(&hist[key8[i]], 1u);   // rank, costliest first
+        if (zip && r >= K) {
+            const unsigned q = r - K;
+            r = K + (q < (n2 + 1u) / 2u ? 2u * q : 2u * (n2 - 1u - q) + 1u);
+        }
+        order[extra + r] = i;
+    }
     if (K > 0u) {
         __syncthreads();
         if (tid < K) top[tid] = order[extra + tid];
@@ -552,7 +561,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         if (s_last) {   // every other CTA has finished: build the next launch's order
             __threadfence();
             reorder_blocks(opt.blk_cost, const_cast<unsigned*>(order), per_view, reinterpret_cast<uint8_t*>(stk_storage),
-                           opt.split_k, opt.split_f);
+                           opt.split_k, opt.split_f, opt.zip_order != 0);
         }
     }
 }

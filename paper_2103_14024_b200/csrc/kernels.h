@@ -30,6 +30,9 @@ struct RenderOpts {
     // of 8 warp tiles with 32 / split_f active lanes each (4x4 or 4x2 pixels), so the slowest
     // tiles of the frame have fewer rays; order[-1] holds the number of hand-out positions
     int32_t split_k = 0, split_f = 1;
+    // with blk_cost: blocks after the split ones zipped (costliest, cheapest, 2nd costliest, ...)
+    // so in-kernel image stores over PCIe (po_render_host) spread over the launch
+    int32_t zip_order = 0;
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.

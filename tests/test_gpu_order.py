@@ -43,3 +43,21 @@ def test_image_independent_of_adaptive_order(env, c1_tree):
     s.synchronize()
     for x in (a, b, m[1:2], c):
         assert torch.equal(x, ref)
+
+
+def test_host_render_independent_of_zipped_cost_order(env, c1_tree):
+    """po_render_host (pinned image written by the kernel over PCIe) uses the zipped cost order;
+    its images must equal the device render of the same view bit for bit."""
+    po, torch = env
+    tree = po.tree_from_gen(c1_tree)
+    cams_np = np.concatenate([gen.config_camera("c1", v)[0] for v in (0, 5, 40, 41)])
+    cams = po.cams_tensor(cams_np)
+    fresh = torch.cuda.Stream()
+    with torch.cuda.stream(fresh):
+        ref = po.po_render(tree, cams[3:4], 800, 800, stream=fresh)
+    fresh.synchronize()
+    pinned = torch.empty((1, 800, 800, 3), dtype=torch.float32, pin_memory=True).numpy()
+    s = torch.cuda.Stream()
+    for v in range(4):
+        po.po_render_host(tree, cams_np[v:v + 1], 800, 800, out_host=pinned, stream=s)
+    assert np.array_equal(pinned, ref.cpu().numpy())
