@@ -521,8 +521,16 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
         }
         if (opt.blk_cost != nullptr) {   // this tile's cost (SM cycles) for the next launch's order
             __syncwarp();
-            // a split block's tiles have 1/F of the rays: scaled so it keeps its rank
-            if (lane == 0) atomicMax(opt.blk_cost + rem, ((unsigned)clock() - c_tile) * (split ? (unsigned)opt.split_f : 1u));
+            // a split block's tiles have 1/F of the rays: scaled so it keeps its rank.  The cost
+            // goes to the block AND its 8 neighbours (lanes 0..8): the next view sees the costly
+            // silhouette a block or so away (c3: 234-259 us with the previous view's own block
+            // costs, 210-211 us dilated, 212 us with the view's own costs; DESIGN.md §6.1 v15)
+            // (neighbours get the unscaled cycles, so a split block keeps its own top rank)
+            const unsigned c = __shfl_sync(0xFFFFFFFFu, (unsigned)clock() - c_tile, 0);
+            const int nx = bx + lane % 3 - 1, ny = by + lane / 3 - 1;
+            if (lane < 9 && nx >= 0 && ny >= 0 && nx < (int)bx_n && ny < (int)by_n)
+                atomicMax(opt.blk_cost + (unsigned)ny * bx_n + (unsigned)nx,
+                          lane == 4 && split ? c * (unsigned)opt.split_f : c);
         }
         if (opt.band_done != nullptr) {   // this tile's pixels are stored: count it for its band
             __threadfence();

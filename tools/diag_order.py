@@ -14,11 +14,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import gen  # noqa: E402
 import paper_2103_14024_b200 as po  # noqa: E402
 
-W = H = 800
-BX = BY = 50
-t = gen.scene_c1()
-tree = po.tree_from_gen(t)
-cams = po.cams_tensor(np.concatenate([gen.config_camera("c1", v)[0] for v in range(12)]))
+WL = os.environ.get("WL", "c1")
+if WL == "c3":
+    W, H = 1920, 1080
+    tree = po.tree_from_gen(gen.scene_c3(), payload=po.PO_F16)
+else:
+    W = H = 800
+    tree = po.tree_from_gen(gen.scene_c1())
+BX, BY = (W + 15) // 16, (H + 15) // 16
+cams = po.cams_tensor(np.concatenate([gen.config_camera(WL, v)[0] for v in range(12)]))
 flush_a = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 flush_b = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 centre = None
