@@ -169,15 +169,11 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
     if constexpr ((OPT & kOptGrid) != 0) {
         if (tr.grid != nullptr && D >= 1) {
             const int G2 = G >> 1;
-#if PO_PREF
             // the next box's index entry is loaded as soon as its cell is known, before this
             // box's leaf is shaded, so the entry's latency overlaps the SH-row loads and FMAs
+            // (DESIGN.md §6.1 v16)
             uint2 EF = __ldg(tr.grid + (((size_t)(c[0] >> 1) * G2 + (c[1] >> 1)) * G2 + (c[2] >> 1)));
-#endif
             while (true) {
-#if !PO_PREF
-                const uint2 EF = __ldg(tr.grid + (((size_t)(c[0] >> 1) * G2 + (c[1] >> 1)) * G2 + (c[2] >> 1)));
-#endif
                 const uint32_t E = EF.x;
                 uint32_t e;
                 int shift;
@@ -208,7 +204,6 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
                 }
                 const float texit = fminf(fminf(te[0], te[1]), te[2]);
                 const float tout = fminf(texit, r.tfar);
-#if PO_PREF
                 int nc[3];
                 bool out = false;
 #pragma unroll
@@ -232,28 +227,6 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
                 c[2] = nc[2];
                 EF = EFn;
             }
-#else
-                if ((e >> 30) == kTagLeaf && tout > t) {
-                    if (!vis.on_leaf(e & kIdxMask, t, tout)) return;
-                }
-                if (!(texit < r.tfar)) return;
-                t = texit;
-                int nc[3];
-                bool out = false;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const bool hit = te[k] == texit;
-                    const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;
-                    const int ck = __float2int_rd(fmaf(t, r.dg[k], r.o[k]));
-                    nc[k] = hit ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
-                    out |= hit & ((unsigned)nex >= (unsigned)G);
-                }
-                if (out) return;
-                c[0] = nc[0];
-                c[1] = nc[1];
-                c[2] = nc[2];
-            }
-#endif
             L = 0;   // fall back from the current cell with a fresh descent
         }
     }
