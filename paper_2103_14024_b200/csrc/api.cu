@@ -235,6 +235,55 @@ static cudaError_t build_grid(po_tree* t) {
         }
     };
     rec(0u, 0, 0, 0, 0);
+    // Empty cells also carry their Chebyshev distance (in level-(D-1) cells, capped at 255) to
+    // the nearest occupied cell, so the traversal can leave the empty cube around the ray's
+    // cell in one step when that reaches further than the cell's octree box (DESIGN.md §6.1
+    // v17).  Exact L-infinity distance transform: two raster passes of the 3x3x3 unit-weight
+    // chamfer over a grid padded by one cell of distance 255.
+    {
+        const int P = G2 + 2;
+        std::vector<uint8_t> dist((size_t)P * P * P, 255);
+        auto at = [&](int x, int y, int z) -> size_t { return ((size_t)x * P + y) * P + z; };
+        for (int x = 0; x < G2; ++x)
+            for (int y = 0; y < G2; ++y)
+                for (int z = 0; z < G2; ++z) {
+                    const uint32_t E = g[((size_t)x * G2 + y) * G2 + z].x;
+                    if ((E >> 30) != 0u) dist[at(x + 1, y + 1, z + 1)] = 0;   // node, leaf or coarse leaf
+                }
+        long off[13];
+        int n_off = 0;
+        for (int dx = -1; dx <= 1; ++dx)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dz = -1; dz <= 1; ++dz)
+                    if (dx < 0 || (dx == 0 && (dy < 0 || (dy == 0 && dz < 0)))) off[n_off++] = ((long)dx * P + dy) * P + dz;
+        uint8_t* dp = dist.data();
+        for (int x = 1; x <= G2; ++x)
+            for (int y = 1; y <= G2; ++y) {
+                uint8_t* row = dp + at(x, y, 1);
+                for (int z = 0; z < G2; ++z) {
+                    int m = row[z];
+                    if (m == 0) continue;
+                    for (int k = 0; k < 13; ++k) m = std::min(m, row[z + off[k]] + 1);
+                    row[z] = (uint8_t)std::min(m, 255);
+                }
+            }
+        for (int x = G2; x >= 1; --x)
+            for (int y = G2; y >= 1; --y) {
+                uint8_t* row = dp + at(x, y, 1);
+                for (int z = G2 - 1; z >= 0; --z) {
+                    int m = row[z];
+                    if (m == 0) continue;
+                    for (int k = 0; k < 13; ++k) m = std::min(m, row[z - off[k]] + 1);
+                    row[z] = (uint8_t)std::min(m, 255);
+                }
+            }
+        for (int x = 0; x < G2; ++x)
+            for (int y = 0; y < G2; ++y)
+                for (int z = 0; z < G2; ++z) {
+                    uint2& c = g[((size_t)x * G2 + y) * G2 + z];
+                    if ((c.x >> 30) == 0u) c.x = (c.x & 0xFFu) | ((uint32_t)dist[at(x + 1, y + 1, z + 1)] << 8);
+                }
+    }
     uint2* d = nullptr;
     cudaError_t e = cudaMalloc(&d, g.size() * sizeof(uint2));
     if (e != cudaSuccess) {

@@ -43,7 +43,9 @@ struct DevTree {
     const float4* __restrict__ sg;
     // kOptGrid cell index: one (E, F) pair per level-(D-1) cell, 2^(D-1) per axis, x-major;
     // null when not built.  E = tag << 30 | payload:
-    //   tag 0: empty box, payload = its level          tag 2: a depth-(D-1) leaf (its entry)
+    //   tag 0: empty box, payload = its level (bits 0-7) | Chebyshev distance of the cell to
+    //          the nearest occupied level-(D-1) cell, capped at 255 (bits 8-15)
+    //                                                  tag 2: a depth-(D-1) leaf (its entry)
     //   tag 1: a depth-(D-1) node (child-table entry)  tag 3: a depth-(D-1) node whose leaves
     //   are consecutive in octant order: payload = 8-bit occupancy mask, F = its first leaf, so
     //   a leaf-level cell's entry is F + popc(mask below its octant) -- no child-table load
@@ -191,27 +193,53 @@ __device__ __forceinline__ void traverse(const DevTree& tr, const RayState& r, V
                     shift = 1;
                 } else {
                     e = 0u;
-                    shift = D - (int)(E & kIdxMask);
+                    shift = D - (int)(E & 0xFFu);   // the empty box's level (bits 8-15: Chebyshev distance)
                 }
                 const int size = 1 << shift;
-                int lo[3];
+                int lo[3], hi[3];
                 float te[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
                     lo[k] = c[k] & ~(size - 1);
-                    const int face = (r.dg[k] >= 0.f) ? lo[k] + size : lo[k];
-                    te[k] = plane_t(r, k, face);
+                    hi[k] = lo[k] + size;
+                    te[k] = plane_t(r, k, (r.dg[k] >= 0.f) ? hi[k] : lo[k]);
                 }
-                const float texit = fminf(fminf(te[0], te[1]), te[2]);
+                float texit = fminf(fminf(te[0], te[1]), te[2]);
+                // an empty cell at Chebyshev distance dc from the nearest occupied level-(D-1)
+                // cell lies in an empty cube of (2 dc - 1)^3 such cells: leave that instead of
+                // the octree box when it reaches further (leaves are still entered through their
+                // own faces, so their segments keep the same t values)
+                const int dc = (E >> 30) == 0u ? (int)((E >> 8) & 0xFFu) : 0;
+                if (dc > 1) {
+                    int lo2[3], hi2[3];
+                    float te2[3];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const int cc = c[k] >> 1;
+                        lo2[k] = max(2 * (cc - dc + 1), 0);
+                        hi2[k] = min(2 * (cc + dc), G);
+                        te2[k] = plane_t(r, k, (r.dg[k] >= 0.f) ? hi2[k] : lo2[k]);
+                    }
+                    const float tx2 = fminf(fminf(te2[0], te2[1]), te2[2]);
+                    if (tx2 > texit) {
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            lo[k] = lo2[k];
+                            hi[k] = hi2[k];
+                            te[k] = te2[k];
+                        }
+                        texit = tx2;
+                    }
+                }
                 const float tout = fminf(texit, r.tfar);
                 int nc[3];
                 bool out = false;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
                     const bool hit = te[k] == texit;
-                    const int nex = (r.dg[k] > 0.f) ? lo[k] + size : lo[k] - 1;
+                    const int nex = (r.dg[k] > 0.f) ? hi[k] : lo[k] - 1;
                     const int ck = __float2int_rd(fmaf(texit, r.dg[k], r.o[k]));
-                    nc[k] = hit ? nex : min(max(ck, lo[k]), lo[k] + size - 1);
+                    nc[k] = hit ? nex : min(max(ck, lo[k]), hi[k] - 1);
                     out |= hit & ((unsigned)nex >= (unsigned)G);
                 }
                 const bool cont = (texit < r.tfar) && !out;
