@@ -452,11 +452,12 @@ def run_c4(args):
         if args.ray_order == "tileleaf" and args.ray_sampling == "tile":
             # keep each 8x4 tile's 32 rays together (warp coherence) and order the TILES by
             # the lowest first-entered leaf among their rays (inter-warp locality)
-            ids, _, _ = po.po_trace(gt, rays, max_leaves=1, gamma=0.0, with_nodes=False)
+            ids, cnt, _ = po.po_trace(gt, rays, max_leaves=1, gamma=0.0, with_nodes=False)
             key = ids[:, 0].to(torch.int64)
             key = torch.where(key < 0, torch.full_like(key, 1 << 40), key).view(-1, 32).min(dim=1).values
             order = torch.argsort(key, stable=True)
             rays = rays.view(-1, 32, 6)[order].reshape(-1, 6).contiguous()
+            cnt = cnt.view(-1, 32)[order].reshape(-1)
         if args.ray_order == "leaf":
             # batch preparation: order rays by the first leaf they enter.  The tree structure is
             # fixed during optimisation, so this key is a per-pixel constant; leaves are
@@ -467,7 +468,17 @@ def run_c4(args):
             key = torch.where(key < 0, torch.full_like(key, 1 << 40), key)
             rays = rays[torch.argsort(key, stable=True)].contiguous()
         tgt = po.po_render_rays(gt, rays, gamma=0.0)   # targets: renders of the unperturbed tree
-        batches.append((rays, tgt))
+        gorder = None
+        if args.pass1_order == "costliest":
+            # pass 1 claims the batch's 32-ray groups costliest first: at gamma 0 a ray's leaf
+            # count is a constant of the fixed tree structure, known to the loader
+            if args.ray_order != "tileleaf" or args.ray_sampling != "tile":
+                _, cnt, _ = po.po_trace(gt, rays, max_leaves=1, gamma=0.0, with_nodes=False)
+            n_g = (rays.shape[0] + 31) // 32
+            cost = torch.zeros(n_g * 32, dtype=torch.int32, device=dev)
+            cost[:rays.shape[0]] = cnt
+            gorder = torch.argsort(-cost.view(n_g, 32).max(dim=1).values, stable=True).to(torch.int32)
+        batches.append((rays, tgt, gorder))
     torch.cuda.synchronize()
     gt.destroy()
     opt = OctreeOptimizer(tree, lr=args.lr, gamma=0.0, device=dev, chunks=args.chunks, max_seg=args.max_seg,
@@ -475,7 +486,7 @@ def run_c4(args):
                           fused_sgd=not args.unfused_sgd)
     # algorithmic bytes of the dominant kernel (k_backward, pass 2 with aux) over the timed batches
     visits = nodes = 0
-    for rays, _ in batches[args.warmup:]:
+    for rays, _, _ in batches[args.warmup:]:
         _, cnt, nd = po.po_trace(tree, rays, max_leaves=0, gamma=0.0)
         visits += int(cnt.sum().item())
         nodes += int(nd.sum().item())
@@ -513,7 +524,8 @@ def run_c4(args):
     # e2e: the same steps through the public API from pinned HOST batches: every step copies its
     # rays + targets host -> device inside the timed region and reads the loss back (D2H)
     e2e_steps = min(K, 10)
-    host = [(b[0].cpu().pin_memory(), b[1].cpu().pin_memory()) for b in batches[args.warmup:args.warmup + e2e_steps]]
+    host = [(b[0].cpu().pin_memory(), b[1].cpu().pin_memory(), None if b[2] is None else b[2].cpu().pin_memory())
+            for b in batches[args.warmup:args.warmup + e2e_steps]]
     opt.train_from_host(host[:2])   # untimed: allocates the pipeline's buffers and side stream
     host_losses = opt.train_from_host(host)   # untimed warm-up of the full-length call
     torch.cuda.synchronize()
@@ -551,7 +563,11 @@ def run_c4(args):
                                    "tree replicated, bucketed NCCL SUM allreduce",
                        "ray_sampling": args.ray_sampling + ("" if args.ray_sampling == "tile" or not args.unsorted
                                                            else " (unsorted)"),
-                       "ray_order": args.ray_order, "pass2_chunks": opt.n_chunks(),
+                       "ray_order": args.ray_order,
+                       "pass1_claim_order": ("32-ray groups costliest first (per-group max leaf count at gamma 0, a "
+                                             "per-pixel constant of the fixed structure, computed by the batch loader)"
+                                             if args.pass1_order == "costliest" else "batch order"),
+                       "pass2_chunks": opt.n_chunks(),
                        "pass2_reduction": "deterministic segmented" if args.deterministic else "atomic",
                        "gradient_sync": ("reduce-scatter + shard SGD + all-gather" if opt.reduce_scatter else
                                          ("allreduce overlapped with pass-2 chunks" if opt.n_chunks() > 1 else
@@ -575,9 +591,10 @@ def run_c4(args):
                                                "(pass 2 replays 32-B stored segment records instead of re-reading "
                                                "the tree)"},
             "gpu_launches": int(launches), "clocks": clk,
-            "e2e": {"value": round(e2e_value, 1), "unit": "rays/s", "h2d_bytes_per_step": n_rays * (24 + 12),
+            "e2e": {"value": round(e2e_value, 1), "unit": "rays/s",
+                    "h2d_bytes_per_step": n_rays * (24 + 12) + (4 * ((n_rays + 31) // 32) if args.pass1_order == "costliest" else 0),
                     "d2h_bytes_per_step": 8, "entry": "OctreeOptimizer.train_from_host on pinned host batches (every step's "
-                                                      "rays + targets copied H2D on a side stream overlapping the "
+                                                      "rays + targets (+ pass-1 group order) copied H2D on a side stream overlapping the "
                                                       "previous step; every step's loss copied D2H, async)"},
         }
         print(json.dumps(line), flush=True)
@@ -675,6 +692,8 @@ def main():
                     help="c4: pass-2 chunks overlapped with the allreduce (default 4 if N>1, else 1)")
     ap.add_argument("--lr", type=float, default=3.0, help="c4: SGD learning rate (loss is a sum over rays)")
     ap.add_argument("--unsorted", action="store_true", help="c4: keep the sampled ray order (no Morton sort)")
+    ap.add_argument("--pass1-order", choices=["costliest", "none"], default="costliest",
+                    help="c4: order in which pass 1 claims the 32-ray groups (po_render_rays_ordered)")
     ap.add_argument("--ray-order", choices=["sampled", "leaf", "tileleaf"], default="tileleaf",
                     help="c4: keep the sampled order, sort the rays by first-entered leaf, or keep each 8x4 "
                          "tile's rays together and sort the tiles by their lowest first-entered leaf")

@@ -219,6 +219,17 @@ po_status po_render_rays(const po_tree* tree, const float* rays, int64_t n, cons
                          float* out_rgb, double* aux, uint32_t* leaf_span, const po_segments* segments,
                          po_stream stream);
 
+/* po_render_rays with a processing order: group_order = device int32[ceil(n/32)], a permutation
+ * of the groups of 32 consecutive rays (group g = rays [32g, 32g+32)); warps claim the groups
+ * in that order.  Scheduling only: every output is the same as po_render_rays' (bitwise).  A
+ * batch whose costliest groups come first ends without a tail of long groups started late
+ * (c4 pass 1 at gamma 0: the per-ray leaf count is a constant of the fixed tree structure,
+ * DESIGN.md §6.2).  group_order must be a permutation (not checked: rays of groups it omits are
+ * not rendered).  NULL = po_render_rays. */
+po_status po_render_rays_ordered(const po_tree* tree, const float* rays, int64_t n, const po_render_opts* opts,
+                                 const int32_t* group_order, float* out_rgb, double* aux, uint32_t* leaf_span,
+                                 const po_segments* segments, po_stream stream);
+
 /* ---- a7/a8: analytic backward (App. B.3: P:886-892 colour, P:938-947 density,
  * P:949-957 two passes, P:959-963 ReLU) -----------------------------------------------
  * dL_dC       device float[n][3], the loss gradient per ray (e.g. 2(C^ - C) for Eq. 3).

@@ -26,7 +26,7 @@ STATUS = {0: "PO_OK", 1: "PO_ERR_INVALID_ARG", 2: "PO_ERR_INVALID_TREE", 3: "PO_
 
 EXPORTS = ["po_last_error", "po_version", "po_launch_count", "po_tree_create", "po_tree_convert", "po_tree_destroy",
            "po_tree_info", "po_tree_index_bytes", "po_tree_write_leaves", "po_tree_set_sg_basis", "po_tree_leaf_payload",
-           "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays",
+           "po_tree_read_leaves", "po_render", "po_render_shard", "po_render_host", "po_camera_rays", "po_render_rays", "po_render_rays_ordered",
            "po_render_backward", "po_render_backward_sgd", "po_backward_plan", "po_render_backward_chunk", "po_render_backward_deterministic",
            "po_render_depth", "po_leaf_max_alpha", "po_l2_loss_grad", "po_tree_sgd_step", "po_tree_sgd_step_range", "po_trace", "po_render_stats",
            "po_render_timeline", "po_ray_step_timing", "po_set_block_order"]
@@ -98,6 +98,7 @@ def lib():
         L.po_render_shard.argtypes = [P, P, I32, I32, I32, P, I32, I32, P, P]
         L.po_render_host.argtypes = [P, P, I32, I32, I32, P, P, P]
         L.po_render_rays.argtypes = [P, P, I64, P, P, P, P, P, P]
+        L.po_render_rays_ordered.argtypes = [P, P, I64, P, P, P, P, P, P, P]
         L.po_backward_plan.argtypes = [P, P, I64, I32, P, P, P, P, P, P]
         L.po_render_backward_chunk.argtypes = [P, P, P, P, I32, P, P, P, P, P, P, P]
         L.po_camera_rays.argtypes = [P, I32, I32, I32, P, I32, P]
@@ -331,9 +332,11 @@ def po_camera_rays(cams, W: int, H: int, stream=None):
 
 
 def po_render_rays(tree: PlenOctree, rays, out=None, aux=None, gamma: float = 0.01, background=(1.0, 1.0, 1.0),
-                   stream=None, leaf_span=None, segments=None):
+                   stream=None, leaf_span=None, segments=None, group_order=None):
     """leaf_span: optional int32 [n][2] tensor (the ABI's uint32 pairs; needs aux) for po_backward_plan;
-    segments: optional Segments(n, max_seg) written for the stored-segment pass 2 (needs aux)."""
+    segments: optional Segments(n, max_seg) written for the stored-segment pass 2 (needs aux);
+    group_order: optional int32 [ceil(n/32)] permutation of the 32-ray groups, the order warps
+    claim them (po_render_rays_ordered; outputs unchanged)."""
     import torch
     rays = _need(rays, torch.float32, (6,))
     n = rays.shape[0]
@@ -345,6 +348,13 @@ def po_render_rays(tree: PlenOctree, rays, out=None, aux=None, gamma: float = 0.
     if leaf_span is not None:
         _need(leaf_span, torch.int32, (2,))
     o = _opts(gamma, background)
+    if group_order is not None:
+        _need(group_order, torch.int32)
+        if group_order.numel() != (n + 31) // 32:
+            raise ValueError("group_order needs ceil(n/32) entries")
+        _check(lib().po_render_rays_ordered(tree.handle, _ptr(rays), n, ctypes.byref(o), _ptr(group_order), _ptr(out),
+                                            _ptr(aux), _ptr(leaf_span), _seg(segments), _stream(stream)))
+        return out
     _check(lib().po_render_rays(tree.handle, _ptr(rays), n, ctypes.byref(o), _ptr(out), _ptr(aux), _ptr(leaf_span),
                                 _seg(segments), _stream(stream)))
     return out

@@ -1057,9 +1057,17 @@ static po_status check_segments(const po_segments* sg, int64_t n_expect, const v
 
 po_status po_render_rays(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts, float* out_rgb,
                          double* aux, uint32_t* leaf_span, const po_segments* segments, po_stream stream) {
+    return po_render_rays_ordered(t, rays, n, opts, nullptr, out_rgb, aux, leaf_span, segments, stream);
+}
+
+po_status po_render_rays_ordered(const po_tree* t, const float* rays, int64_t n, const po_render_opts* opts,
+                                 const int32_t* group_order, float* out_rgb, double* aux, uint32_t* leaf_span,
+                                 const po_segments* segments, po_stream stream) {
     if (po_status s = check_tree(t)) return s;
     po::RenderOpts o;
     if (po_status s = check_opts(opts, &o)) return s;
+    if (n > (int64_t)INT32_MAX * 32) return fail(PO_ERR_INVALID_ARG, "n too large for 32-ray groups");
+    o.group_order = group_order;
     if (n < 0) return fail(PO_ERR_INVALID_ARG, "n < 0");
     if (leaf_span && !aux) return fail(PO_ERR_INVALID_ARG, "leaf_span needs aux (pass-1 mode)");
     if (leaf_span && ((uintptr_t)leaf_span & 7u) != 0) return fail(PO_ERR_INVALID_ARG, "leaf_span not 8-byte aligned");

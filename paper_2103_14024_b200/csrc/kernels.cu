@@ -653,8 +653,8 @@ __global__ void __launch_bounds__(256, 2) k_render_rays_p(DevTree tr, const floa
         unsigned c = 0;
         if (lane == 0) c = atomicAdd(work, 1u);
         c = __shfl_sync(0xffffffffu, c, 0);
-        const int64_t i0 = (int64_t)c * 32;
-        if (i0 >= n) break;
+        if ((int64_t)c * 32 >= n) break;
+        const int64_t i0 = 32 * (int64_t)(opt.group_order != nullptr ? __ldg(opt.group_order + c) : (int32_t)c);
         if (i0 + lane < n) render_ray<DEG, F16>(tr, rays, i0 + lane, opt, out, aux, span, so, stk);
         __syncwarp();
     }

@@ -33,6 +33,9 @@ struct RenderOpts {
     // with blk_cost: blocks after the split ones zipped (costliest, cheapest, 2nd costliest, ...)
     // so in-kernel image stores over PCIe (po_render_host) spread over the launch
     int32_t zip_order = 0;
+    // k_render_rays_p only: NULL, or device int32[ceil(n/32)], a permutation of the 32-ray groups
+    // giving the order in which warps claim them (scheduling only; outputs stay per ray)
+    const int32_t* group_order = nullptr;
 };
 
 // work: 2 device uint32 counters, zero on entry, reset to zero by the kernel on exit.

@@ -93,7 +93,7 @@ class OctreeOptimizer:
         return 4 if self.world_size > 1 else 1
 
     def train_from_host(self, host_batches) -> torch.Tensor:
-        """Steps over (rays [n][6], target [n][3]) batches in PINNED host memory, one step each.
+        """Steps over (rays [n][6], target [n][3][, group_order]) batches in PINNED host memory, one step each.
 
         Batch i+1's host->device copy runs on a side stream while step i computes (two device
         buffers, each refilled only after the step that read it), and every step's loss is
@@ -111,8 +111,10 @@ class OctreeOptimizer:
         if key not in self._bufs:
             self._bufs[key] = (torch.cuda.Stream(self.device),
                                [(torch.empty((n, 6), dtype=torch.float32, device=self.device),
-                                 torch.empty((n, 3), dtype=torch.float32, device=self.device)) for _ in range(2)],
+                                 torch.empty((n, 3), dtype=torch.float32, device=self.device),
+                                 torch.empty((n + 31) // 32, dtype=torch.int32, device=self.device)) for _ in range(2)],
                                [torch.cuda.Event() for _ in range(2)])
+        ordered = len(host_batches[0]) > 2 and host_batches[0][2] is not None
         copy, bufs, ready = self._bufs[key]
         if ("losses", k) not in self._bufs:
             self._bufs[("losses", k)] = torch.empty(k, dtype=torch.float64, pin_memory=True)
@@ -128,6 +130,8 @@ class OctreeOptimizer:
                     copy.wait_event(free[b])   # step i-2 has finished reading buffer b
                 bufs[b][0].copy_(host_batches[i][0], non_blocking=True)
                 bufs[b][1].copy_(host_batches[i][1], non_blocking=True)
+                if ordered:
+                    bufs[b][2].copy_(host_batches[i][2], non_blocking=True)
                 ready[b].record(copy)
 
         prefetch(0)
@@ -136,19 +140,21 @@ class OctreeOptimizer:
                 prefetch(i + 1)
             b = i % 2
             main.wait_event(ready[b])
-            loss = self.step(bufs[b][0], bufs[b][1])
+            loss = self.step(bufs[b][0], bufs[b][1], bufs[b][2] if ordered else None)
             free[b] = torch.cuda.Event()
             free[b].record(main)
             losses[i].copy_(loss.view(()), non_blocking=True)
         return losses
 
-    def step(self, rays: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
-        """rays [n][6] f32, target [n][3] f32 on this rank's device; returns the local loss (device f64)."""
+    def step(self, rays: torch.Tensor, target: torch.Tensor, group_order=None) -> torch.Tensor:
+        """rays [n][6] f32, target [n][3] f32 on this rank's device; returns the local loss (device f64).
+        group_order: optional int32 [ceil(n/32)] order in which pass 1 claims the batch's 32-ray
+        groups (costliest first removes pass 1's tail; scheduling only)."""
         n = rays.shape[0]
         rgb, aux, dL, span, perm, seg = self._buffers(n)
         K = self.n_chunks()
         po_render_rays(self.tree, rays, out=rgb, aux=aux, gamma=self.gamma, background=self.background,
-                       leaf_span=span if K > 1 else None, segments=seg)
+                       leaf_span=span if K > 1 else None, segments=seg, group_order=group_order)
         po_l2_loss_grad(rgb, target, dL_dC=dL, loss=self.loss)
         # the gradient buffer is zero here: it starts zeroed and every SGD call below zeroes
         # what it consumed (PO_SGD_ZERO_GRAD), which replaces a 0.7 GB memset per step
