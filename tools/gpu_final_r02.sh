@@ -4,7 +4,7 @@
 # --set full captures (with lts__t_bytes) of the c1 / c3 render, c4 pass 1 and replay, the 2-rank
 # paths, compute-sanitizer, the per-config oracle baselines and the L2 micro-benchmark.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-O=gpurun_out/final; mkdir -p $O
+O=gpurun_out/${TAG:-final}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt 2>&1
 python -c 'import __graft_entry__ as g; g.build()' > $O/build.log 2>&1 || { echo BUILD FAILED; tail -30 $O/build.log; exit 1; }
 if [ "${SKIP_TESTS:-0}" != "1" ]; then
