@@ -84,6 +84,9 @@ struct po_tree {
     std::vector<uint32_t> h_child;   // the caller's child table as given (po_tree_convert)
     uint2* d_grid = nullptr;         // dense level-(D-1) cell index (build_grid, at po_tree_create)
     size_t grid_bytes = 0;
+    // the smallest box of level-(D-1) cells holding every occupied cell (leaf units; the whole
+    // cube without an index): rays are clipped to it (DESIGN.md §6.1 v18)
+    int occ_lo[3] = {-1, -1, -1}, occ_hi[3] = {-1, -1, -1};
     // po_render_host holds this for its whole body (camera / image / pipeline scratch)
     std::mutex host_mu;
     static constexpr int64_t kPayloadPad = 4096;   // spare zero leaves after the payload arrays
@@ -284,6 +287,24 @@ static cudaError_t build_grid(po_tree* t) {
                     if ((c.x >> 30) == 0u) c.x = (c.x & 0xFFu) | ((uint32_t)dist[at(x + 1, y + 1, z + 1)] << 8);
                 }
     }
+    {   // occupied bounding box (level-(D-1) cells, in leaf units); an empty tree keeps the cube
+        int lo[3] = {G2, G2, G2}, hi[3] = {-1, -1, -1};
+        for (int x = 0; x < G2; ++x)
+            for (int y = 0; y < G2; ++y)
+                for (int z = 0; z < G2; ++z)
+                    if ((g[((size_t)x * G2 + y) * G2 + z].x >> 30) != 0u) {
+                        const int v[3] = {x, y, z};
+                        for (int k = 0; k < 3; ++k) {
+                            lo[k] = std::min(lo[k], v[k]);
+                            hi[k] = std::max(hi[k], v[k]);
+                        }
+                    }
+        if (hi[0] >= 0)
+            for (int k = 0; k < 3; ++k) {
+                t->occ_lo[k] = 2 * lo[k];
+                t->occ_hi[k] = 2 * (hi[k] + 1);
+            }
+    }
     uint2* d = nullptr;
     cudaError_t e = cudaMalloc(&d, g.size() * sizeof(uint2));
     if (e != cudaSuccess) {
@@ -312,6 +333,11 @@ po::DevTree dev_tree(const po_tree* t) {
     d.scale = (float)std::ldexp(1.0, t->desc.max_depth) / t->desc.bbox_edge;
     d.odd_sign = t->desc.sh_sign == PO_SH_NO_CS ? -1.f : 1.f;
     d.sg = t->d_sg;
+    const float G = (float)std::ldexp(1.0, t->desc.max_depth);
+    for (int k = 0; k < 3; ++k) {
+        d.clip_lo[k] = t->occ_lo[k] >= 0 ? (float)t->occ_lo[k] : 0.f;
+        d.clip_hi[k] = t->occ_hi[k] >= 0 ? (float)t->occ_hi[k] : G;
+    }
     return d;
 }
 

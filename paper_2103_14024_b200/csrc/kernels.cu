@@ -1287,7 +1287,7 @@ __global__ void __launch_bounds__(256) k_trace(DevTree tr, const float* __restri
     for (int j = 0; j < max_leaves && ids; ++j) ids[j] = -1;
     TraceVisitor v{tr, 1.f, gamma, ids, ids ? max_leaves : 0, 0, 0};
     RayState r;
-    if (ray_setup(tr, o, d, r)) {
+    if (ray_setup(tr, o, d, r, GRID)) {   // the classic reference walks the whole cube
         if constexpr (GRID) traverse<kOptDefault | kOptGrid>(tr, r, v, stk);
         else traverse<kOptDefault>(tr, r, v, stk);
     }
@@ -1305,7 +1305,7 @@ __global__ void __launch_bounds__(256) k_stats(DevTree tr, const po_camera* __re
         float o[3], d[3];
         camera_ray(cams, blockIdx.z, px, py, o, d);
         RayState r;
-        if (ray_setup(tr, o, d, r)) {
+        if (ray_setup(tr, o, d, r, false)) {   // counts of the classic descent over the whole cube
             StatsVisitor v{tr, 1.f, gamma, 0, 0, 0, 0, 0};
             traverse(tr, r, v, stk);
             v4[0] = v.leaves;

@@ -51,6 +51,10 @@ struct DevTree {
     //   a leaf-level cell's entry is F + popc(mask below its octant) -- no child-table load
     //   0xFFFFFFFF: a leaf coarser than D-1 covers the cell (classic descent)
     const uint2* __restrict__ grid = nullptr;
+    // rays are clipped to this box (leaf units, integral): the occupied cells' bounding box in
+    // level-(D-1) cells when the index is built, else [0, 2^D]^3.  Leaves lie inside it, so
+    // every leaf segment keeps its t values (its faces are the same planes)
+    float clip_lo[3] = {0.f, 0.f, 0.f}, clip_hi[3] = {0.f, 0.f, 0.f};
 };
 
 struct RayState {
@@ -76,7 +80,10 @@ __device__ __forceinline__ bool unit_direction(const float dir[3], float d[3]) {
     return true;
 }
 
-__device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], const float dir[3], RayState& r) {
+// clip = false: the whole cube [0, 2^D]^3 (the classic reference descent of k_trace / k_stats,
+// whose node counts define SURVEY 8(d)'s algorithmic bytes); true: the occupied box clip_lo/hi.
+__device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], const float dir[3], RayState& r,
+                                          bool clip = true) {
     // a zero or non-finite direction renders the background
     if (!unit_direction(dir, r.d)) return false;
     const float G = (float)(1 << tr.depth);
@@ -85,15 +92,16 @@ __device__ __forceinline__ bool ray_setup(const DevTree& tr, const float o[3], c
     for (int k = 0; k < 3; ++k) {
         r.o[k] = (o[k] - tr.bmin[k]) * tr.scale;
         r.dg[k] = r.d[k] * tr.scale;
+        const float lo = clip ? tr.clip_lo[k] : 0.f, hi = clip ? tr.clip_hi[k] : G;
         if (r.dg[k] != 0.f) {
             r.inv[k] = 1.0f / r.dg[k];
-            float ta = (0.f - r.o[k]) * r.inv[k];
-            float tb = (G - r.o[k]) * r.inv[k];
+            float ta = (lo - r.o[k]) * r.inv[k];   // plane_t's expression
+            float tb = (hi - r.o[k]) * r.inv[k];
             tn = fmaxf(tn, fminf(ta, tb));
             tf = fminf(tf, fmaxf(ta, tb));
         } else {
             r.inv[k] = INFINITY;
-            if (!(r.o[k] >= 0.f && r.o[k] <= G)) return false;
+            if (!(r.o[k] >= lo && r.o[k] <= hi)) return false;
         }
     }
     r.tnear = tn;
