@@ -1305,13 +1305,20 @@ po_status po_render_backward_deterministic(const po_tree* tc, const float* rays,
     const size_t a4 = ((size_t)std::max<int64_t>(S, 1) * 4 + 255) / 256 * 256;
     const size_t need = 2 * a1 + scan_bytes + 5 * a4 + 4 * a4 + sort_bytes;
     if (t->det_cap < need) {   // keep cnt / offs: grow into a fresh block and copy offs over
+        // 25 % headroom: batches of one scene vary by a few % in segment count, and every
+        // regrowth frees (a device-wide sync) and reallocates hundreds of MB inside the step
+        size_t got = need + need / 4;
         void* nb = nullptr;
-        if ((e = cudaMalloc(&nb, need)) != cudaSuccess) return cuda_status(e, "scratch");
+        if ((e = cudaMalloc(&nb, got)) != cudaSuccess) {
+            (void)cudaGetLastError();
+            got = need;
+            if ((e = cudaMalloc(&nb, got)) != cudaSuccess) return cuda_status(e, "scratch");
+        }
         e = cudaMemcpyAsync(static_cast<char*>(nb) + a1, offs, (size_t)(n + 1) * 4, cudaMemcpyDeviceToDevice, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         cudaFree(t->d_det);
         t->d_det = nb;
-        t->det_cap = need;
+        t->det_cap = got;
         if (e != cudaSuccess) return cuda_status(e, "scratch copy");
         offs = reinterpret_cast<int32_t*>(static_cast<char*>(t->d_det) + a1);
     }
