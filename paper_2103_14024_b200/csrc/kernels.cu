@@ -33,7 +33,7 @@ struct FwdVisitor {
         C[0] = C[1] = C[2] = 0.f;
     }
     __device__ __forceinline__ void on_node() {}
-    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+    __device__ __forceinline__ bool shade(uint32_t idx, float t0, float t1) {
         const float st = __ldg(tr.sigma + idx);
         float z[3];
         sh_dot<DEG, F16>(tr, idx, Y, z);   // row loads issued together with the sigma load
@@ -44,6 +44,37 @@ struct FwdVisitor {
         T = a.Tn;
         return !(T < gamma);
     }
+#if PO_DEFER
+    // deferred leaf: a leaf's sigma~ and SH row are prefetched into L1 when it is reached and
+    // composited when the next leaf is reached (or the ray ends), so the row latency overlaps
+    // the box steps in between; same compositing order and values (the early stop is decided
+    // one leaf later, and the leaf after a stopping one is never composited)
+    uint32_t pidx = 0xFFFFFFFFu;
+    float pt0 = 0.f, pt1 = 0.f;
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
+        if (pidx != 0xFFFFFFFFu && !shade(pidx, pt0, pt1)) {
+            pidx = 0xFFFFFFFFu;
+            return false;
+        }
+        const char* row = static_cast<const char*>(tr.sh) + (uint64_t)idx * (uint32_t)tr.sh_row * (F16 ? 2u : 4u);
+        constexpr int RB = F16 ? 6 * ShDim<DEG>::B : 12 * ShDim<DEG>::B;   // row bytes
+#pragma unroll
+        for (int off = 0; off < RB; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + off));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(row + RB - 1));   // rows are 16-B, not line, aligned
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tr.sigma + idx));
+        pidx = idx;
+        pt0 = t0;
+        pt1 = t1;
+        return true;
+    }
+    __device__ __forceinline__ void finish() {
+        if (pidx != 0xFFFFFFFFu) shade(pidx, pt0, pt1);
+        pidx = 0xFFFFFFFFu;
+    }
+#else
+    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) { return shade(idx, t0, t1); }
+    __device__ __forceinline__ void finish() {}
+#endif
 };
 
 // Stored pass-1 segments (po_segments): record k of ray i = two float4 at (k n + i) * 2:
@@ -506,6 +537,7 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                 {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
                     traverse<OPT & (kOptLean | kOptGrid)>(tr, r, v, stk);
+                    v.finish();
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -592,6 +624,7 @@ __device__ __forceinline__ void render_ray(const DevTree& tr, const float* __res
         if (hit) {
             FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
             traverse<kOptDefault | kOptGrid>(tr, r, v, stk);   // cell index when built
+            v.finish();
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
         }
