@@ -44,37 +44,8 @@ struct FwdVisitor {
         T = a.Tn;
         return !(T < gamma);
     }
-#if PO_DEFER
-    // deferred leaf: a leaf's sigma~ and SH row are prefetched into L1 when it is reached and
-    // composited when the next leaf is reached (or the ray ends), so the row latency overlaps
-    // the box steps in between; same compositing order and values (the early stop is decided
-    // one leaf later, and the leaf after a stopping one is never composited)
-    uint32_t pidx = 0xFFFFFFFFu;
-    float pt0 = 0.f, pt1 = 0.f;
-    __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) {
-        if (pidx != 0xFFFFFFFFu && !shade(pidx, pt0, pt1)) {
-            pidx = 0xFFFFFFFFu;
-            return false;
-        }
-        const char* row = static_cast<const char*>(tr.sh) + (uint64_t)idx * (uint32_t)tr.sh_row * (F16 ? 2u : 4u);
-        constexpr int RB = F16 ? 6 * ShDim<DEG>::B : 12 * ShDim<DEG>::B;   // row bytes
-#pragma unroll
-        for (int off = 0; off < RB; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + off));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(row + RB - 1));   // rows are 16-B, not line, aligned
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(tr.sigma + idx));
-        pidx = idx;
-        pt0 = t0;
-        pt1 = t1;
-        return true;
-    }
-    __device__ __forceinline__ void finish() {
-        if (pidx != 0xFFFFFFFFu) shade(pidx, pt0, pt1);
-        pidx = 0xFFFFFFFFu;
-    }
-#else
     __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) { return shade(idx, t0, t1); }
     __device__ __forceinline__ void finish() {}
-#endif
 };
 
 // Stored pass-1 segments (po_segments): record k of ray i = two float4 at (k n + i) * 2:
