@@ -45,7 +45,6 @@ struct FwdVisitor {
         return !(T < gamma);
     }
     __device__ __forceinline__ bool on_leaf(uint32_t idx, float t0, float t1) { return shade(idx, t0, t1); }
-    __device__ __forceinline__ void finish() {}
 };
 
 // Stored pass-1 segments (po_segments): record k of ray i = two float4 at (k n + i) * 2:
@@ -508,7 +507,6 @@ __global__ void __launch_bounds__(256, MINB) k_render(DevTree tr, const po_camer
                 {
                     FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
                     traverse<OPT & (kOptLean | kOptGrid)>(tr, r, v, stk);
-                    v.finish();
 #pragma unroll
                     for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
                 }
@@ -595,7 +593,6 @@ __device__ __forceinline__ void render_ray(const DevTree& tr, const float* __res
         if (hit) {
             FwdVisitor<DEG, F16> v(tr, r.d, opt.gamma);
             traverse<kOptDefault | kOptGrid>(tr, r, v, stk);   // cell index when built
-            v.finish();
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) C[ch] = fmaf(v.T, opt.bg[ch], v.C[ch]);
         }
