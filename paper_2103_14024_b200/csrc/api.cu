@@ -747,8 +747,9 @@ static std::pair<int, int> split_cfg() {
         if (const char* e = getenv("PO_SPLIT_K")) k = atoi(e);
         if (const char* e = getenv("PO_SPLIT_F")) f = atoi(e);
 #endif
+        if (f != 1 && f != 2 && f != 4 && f != 8) f = 1;
         k = k < 0 ? 0 : (k > kSplitMaxK ? kSplitMaxK : k);
-        if (f != 1 && f != 2 && f != 4) f = 1;
+        if (f > 1 && (size_t)k * (f - 1) > kSplitExtra) k = (int)(kSplitExtra / (f - 1));   // table room
         return std::make_pair(f == 1 ? 0 : k, f);
     }();
     return cfg;

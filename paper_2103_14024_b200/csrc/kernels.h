@@ -26,8 +26,8 @@ struct RenderOpts {
     // the last CTA then rewrites `order` (costliest block first) for the next launch on the
     // stream and zeroes the costs again.  `order` must then be a mutable per-stream table.
     unsigned* blk_cost = nullptr;
-    // with blk_cost: the split_k costliest blocks are rendered as split_f (2 or 4) sub-blocks
-    // of 8 warp tiles with 32 / split_f active lanes each (4x4 or 4x2 pixels), so the slowest
+    // with blk_cost: the split_k costliest blocks are rendered as split_f (2, 4 or 8) sub-blocks
+    // of 8 warp tiles with 32 / split_f active lanes each (4x4, 4x2 or 4x1 pixels), so the slowest
     // tiles of the frame have fewer rays; order[-1] holds the number of hand-out positions
     int32_t split_k = 0, split_f = 1;
     // with blk_cost: blocks after the split ones zipped (costliest, cheapest, 2nd costliest, ...)
