@@ -627,3 +627,42 @@ def test_train_from_host_matches_step(env, c0_tree):
     np.testing.assert_allclose(got.numpy(), ref, rtol=1e-5)
     for x, y in zip(trees[0].read_leaves(), trees[1].read_leaves()):
         np.testing.assert_allclose(x, y, rtol=1e-4, atol=1e-5)
+
+
+def test_occupied_box_clip_and_cube_steps(env):
+    """Occupied-box clipping and empty Chebyshev-cube steps (DESIGN.md §6.1 v17-v18) on a tree
+    whose leaves fill one off-centre slab of a depth-6 grid: origins inside the cube but outside
+    the slab's box, axis-aligned rays on the box's faces and edges, random rays.  The production
+    traversal (clipped, cubes) must give the classic whole-cube descent's leaf sequences on every
+    ray and bit-identical colours to the same tree without an index; tie-free rays match the
+    oracle at RGB_TOL."""
+    po, om, torch = env
+    D = 6
+    xs, ys, zs = np.meshgrid(np.arange(40, 52), np.arange(8, 20), np.arange(30, 33), indexing="ij")
+    cells = np.stack([xs.ravel(), ys.ravel(), zs.ravel()], 1)
+    child, order = gen.build_from_leaf_cells(cells, D)
+    sig, sh = gen.make_payload_random(rng(77), cells.shape[0], 1, sigma_scale=2.0)
+    t = gen.Tree(depth=D, bbox_min=np.array([-1.0, -1.0, -1.0], np.float32), edge=2.0, sh_degree=1, child=child,
+                 sigma=sig, sh=sh)
+    tree = po.tree_from_gen(t)
+    plain = po.tree_from_gen(t, index=False)
+    u = 2.0 / (1 << D)   # world size of one leaf cell
+    w = lambda c: -1.0 + c * u   # noqa: E731  leaf-grid plane -> world coordinate
+    axis = []
+    for (y, z) in ((8, 30), (20, 33), (14, 31.5), (8, 31.5), (14, 30)):   # faces, edges, interior
+        axis += [[-0.999, w(y), w(z), 1, 0, 0], [0.999, w(y), w(z), -1, 0, 0]]
+    for (x, z) in ((40, 30), (52, 33), (46, 31.5)):
+        axis += [[w(x), -0.999, w(z), 0, 1, 0], [w(x), 0.999, w(z), 0, -1, 0]]
+    for (x, y) in ((40, 8), (52, 20), (46, 14), (45.5, 13.5)):
+        axis += [[w(x), w(y), -0.999, 0, 0, 1], [w(x), w(y), 0.999, 0, 0, -1]]
+    rays = np.concatenate([np.array(axis, np.float32), gen.random_rays(78, 20000, inside_frac=0.6)])
+    rd = _dev(torch, rays)
+    for gamma in (0.01, 0.0):
+        a = po.po_trace(tree, rd, max_leaves=64, gamma=gamma, with_nodes=False)
+        b = po.po_trace(tree, rd, max_leaves=64, gamma=gamma, with_nodes=False, classic=True)
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        ca = po.po_render_rays(tree, rd, gamma=gamma)
+        assert torch.equal(ca, po.po_render_rays(plain, rd, gamma=gamma))
+        ot = om.OracleTree(t)
+        ref = om.render(ot, rays.astype(np.float64), gamma=gamma)
+        _check_rgb(om, ot, rays.astype(np.float64), gamma, ca.cpu().numpy(), ref["rgb"], 0.9)
