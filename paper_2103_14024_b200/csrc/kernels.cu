@@ -1054,7 +1054,10 @@ struct SgdSink {
 };
 
 template <int DEG>
-__global__ void __launch_bounds__(256, 3) k_backward_replay_sgd(DevTree tr, const float* __restrict__ rays, int64_t n,
+#ifndef PO_REPLAY_MINB
+#define PO_REPLAY_MINB 4   // 4 CTAs/SM (64 registers, 104-B spill) measured +1.2 % over 3 (80, none): DESIGN.md §6.2
+#endif
+__global__ void __launch_bounds__(256, PO_REPLAY_MINB) k_backward_replay_sgd(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                              const float* __restrict__ dL_dC,
                                                              const double* __restrict__ aux, SegIn si,
                                                              float* __restrict__ sigma, float* __restrict__ sh,
