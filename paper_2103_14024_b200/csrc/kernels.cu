@@ -644,7 +644,10 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(DevTree tr, const float*
 // CTA's slot until its slowest warp ends: at gamma = 0 the ray lengths vary widely).  work[0] =
 // next chunk, work[1] = finished CTAs; both zero on entry, reset by the last CTA.
 template <int DEG, bool F16>
-__global__ void __launch_bounds__(256, 2) k_render_rays_p(DevTree tr, const float* __restrict__ rays, int64_t n,
+#ifndef PO_RAYS_MINB
+#define PO_RAYS_MINB 2
+#endif
+__global__ void __launch_bounds__(256, PO_RAYS_MINB) k_render_rays_p(DevTree tr, const float* __restrict__ rays, int64_t n,
                                                        RenderOpts opt, float* __restrict__ out,
                                                        double* __restrict__ aux, uint32_t* __restrict__ span,
                                                        SegOut so, unsigned* __restrict__ work) {
