@@ -147,7 +147,7 @@ po_status po_tree_read_leaves(const po_tree* tree, float* sigma, float* sh);
  * (after compositing that segment, reading Q11), then C += T c_N.
  * Scheduling (no effect on pixel values): a single-view render hands its 16x16 blocks out
  * costliest first by the per-block costs the previous single-view render of the same W x H on
- * the same stream measured, the 8 costliest split into 16-lane tiles (the first render on a
+ * the same stream measured, the 32 costliest split into 16-lane tiles (the first render on a
  * stream: centre-out).  The first single-view render of a size on a stream allocates that
  * stream's order table (8 B per block + 772 B; PO_ERR_OOM if that fails); up to 256 streams per
  * tree (PO_ERR_UNSUPPORTED beyond). */

@@ -742,7 +742,7 @@ static unsigned* stream_order_table(po_tree* t, cudaStream_t s, int W, int H, co
 // warp tile (DESIGN.md §6.1 v14); PO_SPLIT_K / PO_SPLIT_F override it in diagnostics builds.
 static std::pair<int, int> split_cfg() {
     static const std::pair<int, int> cfg = [] {
-        int k = 8, f = 2;
+        int k = 32, f = 2;
 #ifdef PO_DIAG
         if (const char* e = getenv("PO_SPLIT_K")) k = atoi(e);
         if (const char* e = getenv("PO_SPLIT_F")) f = atoi(e);
